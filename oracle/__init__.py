@@ -1,0 +1,130 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY (see oracle/zz_oracle.c header).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module.  It wraps the plain C column-by-column robust substitution with ctypes.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libzzoracle.so")
+_lib = None
+
+
+def build(force=False):
+    src = os.path.join(_HERE, "zz_oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-o", _SO, src, "-lm"])
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        vp, ci, cd = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        lib.zzo_protect_update.restype = ci
+        lib.zzo_protect_update.argtypes = [cd, cd, cd]
+        lib.zzo_protect_division.restype = ci
+        lib.zzo_protect_division.argtypes = [cd, cd]
+        lib.zzo_blocks.restype = ci
+        lib.zzo_blocks.argtypes = [ci, vp, ci, vp, vp]
+        lib.zzo_eig_pairs.restype = ci
+        lib.zzo_eig_pairs.argtypes = [ci, vp, ci, vp, ci, vp, vp, vp, vp]
+        lib.zzo_tgevc_ex.restype = ci
+        lib.zzo_tgevc_ex.argtypes = [ci, vp, ci, vp, ci, vp, vp, ci, vp, vp, vp, vp, ci, ci]
+        lib.zzo_count_columns.restype = ci
+        lib.zzo_count_columns.argtypes = [ci, vp, ci, vp]
+        lib.zzo_flops.restype = cd
+        lib.zzo_flops.argtypes = [ci, vp, ci, vp]
+        _lib = lib
+    return _lib
+
+
+def _f(A):
+    A = np.asarray(A, dtype=np.float64)
+    if A.ndim != 2 or not A.flags.f_contiguous:
+        A = np.asfortranarray(A, dtype=np.float64)
+    return A
+
+
+def _sel(select, m):
+    if select is None:
+        return None
+    s = np.ascontiguousarray(np.asarray(select, dtype=np.int32).reshape(-1))
+    assert s.size == m
+    return s
+
+
+def protect_update(y, t, x):
+    """exponent e of xi = 2^e = ProtectUpdate(y, t, x)"""
+    return _load().zzo_protect_update(y, t, x)
+
+
+def protect_division(b, t):
+    """exponent e of xi = 2^e = ProtectDivision(b, t)"""
+    return _load().zzo_protect_division(b, t)
+
+
+def blocks(S):
+    S = _f(S)
+    m = S.shape[0]
+    bs = np.zeros(max(m, 1), np.int32)
+    bz = np.zeros(max(m, 1), np.int32)
+    n = _load().zzo_blocks(m, S.ctypes.data, max(m, 1), bs.ctypes.data, bz.ctypes.data)
+    if n < 0:
+        raise ValueError("status %d" % n)
+    return bs[:n].copy(), bz[:n].copy()
+
+
+def eig_pairs(S, T):
+    """per-row normalised (a, b, beta, kind) and the status"""
+    S, T = _f(S), _f(T)
+    m = S.shape[0]
+    a, b, be = (np.zeros(max(m, 1)) for _ in range(3))
+    kd = np.zeros(max(m, 1), np.int32)
+    st = _load().zzo_eig_pairs(m, S.ctypes.data, max(m, 1), T.ctypes.data, max(m, 1), a.ctypes.data,
+                               b.ctypes.data, be.ctypes.data, kd.ctypes.data)
+    return a[:m], b[:m], be[:m], kd[:m], st
+
+
+def count_columns(S, select=None):
+    S = _f(S)
+    m = S.shape[0]
+    sel = _sel(select, m)
+    return _load().zzo_count_columns(m, S.ctypes.data, max(m, 1), None if sel is None else sel.ctypes.data)
+
+
+def flops(S, select=None):
+    """nominal F(select) = sum_c 2 r_c (r_c - 1)"""
+    S = _f(S)
+    m = S.shape[0]
+    sel = _sel(select, m)
+    return _load().zzo_flops(m, S.ctypes.data, max(m, 1), None if sel is None else sel.ctypes.data)
+
+
+def tgevc(S, T, select=None, protect=True, nthreads=0):
+    """Robust column-by-column eigenvectors.  Returns dict(X, e, logmax, pairs, stats, status);
+    X is m x n_sel column-major, e the int32 col_scale_exp, logmax L_c, pairs (m,3)."""
+    S, T = _f(S), _f(T)
+    m = S.shape[0]
+    sel = _sel(select, m)
+    lib = _load()
+    n = lib.zzo_count_columns(m, S.ctypes.data, max(m, 1), None if sel is None else sel.ctypes.data)
+    if n < 0:
+        return dict(X=None, e=None, logmax=None, pairs=None, stats=None, status=n)
+    X = np.zeros((m, max(n, 1)), order="F")
+    e = np.zeros(max(n, 1), np.int32)
+    L = np.zeros(max(n, 1))
+    pairs = np.zeros((max(m, 1), 3))
+    stats = np.zeros(3, np.int32)
+    st = lib.zzo_tgevc_ex(m, S.ctypes.data, max(m, 1), T.ctypes.data, max(m, 1),
+                          None if sel is None else sel.ctypes.data, X.ctypes.data, max(m, 1),
+                          e.ctypes.data, L.ctypes.data, pairs.ctypes.data, stats.ctypes.data,
+                          1 if protect else 0, nthreads)
+    return dict(X=X[:, :n], e=e[:n], logmax=L[:n], pairs=pairs[:m], stats=stats, status=st)

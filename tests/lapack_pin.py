@@ -1,0 +1,45 @@
+"""LAPACK DTGEVC as an independent black-box pin for the oracle (scipy's bundled OpenBLAS
+exports LAPACKE_dtgevc; nothing of it is used by the product path or the oracle)."""
+import ctypes
+import glob
+import os
+
+import numpy as np
+
+_f = None
+
+
+def available():
+    return bool(_paths())
+
+
+def _paths():
+    import scipy
+    base = os.path.dirname(os.path.dirname(scipy.__file__))
+    return glob.glob(os.path.join(base, "scipy.libs", "libscipy_openblas*.so"))
+
+
+def dtgevc(S, T, select=None):
+    """Right eigenvectors (HOWMNY='A' or 'S'); returns (info, VR)."""
+    global _f
+    if _f is None:
+        lib = ctypes.CDLL(_paths()[0])
+        _f = lib.scipy_LAPACKE_dtgevc
+        _f.restype = ctypes.c_int
+    S = np.asfortranarray(S, dtype=np.float64)
+    T = np.asfortranarray(T, dtype=np.float64)
+    m = S.shape[0]
+    VR = np.zeros((m, max(m, 1)), order="F")
+    VL = np.zeros((1, 1))
+    mo = ctypes.c_int(0)
+    if select is None:
+        how, sel = b"A", None
+    else:
+        how = b"S"
+        sel = np.ascontiguousarray(np.asarray(select, dtype=np.int32))
+    vp = ctypes.c_void_p
+    info = _f(102, ctypes.c_char(b"R"), ctypes.c_char(how),
+              None if sel is None else sel.ctypes.data_as(vp), m, S.ctypes.data_as(vp), m,
+              T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), 1, VR.ctypes.data_as(vp), m, m,
+              ctypes.byref(mo))
+    return info, VR[:, :mo.value]
