@@ -1,0 +1,137 @@
+/*
+ * include/zz.h -- C ABI of the B200-native robust generalized-eigenvector solver.
+ *
+ * Operation.  For a real pencil (S,T) in generalized real Schur form (PAPER.md:56-61:
+ * S quasi-upper-triangular with 1x1 and 2x2 diagonal blocks, T upper triangular) compute
+ * the right generalized eigenvectors, i.e. the columns of V in the homogeneous matrix
+ * equation  S V D - T V B = 0, D diagonal and B block diagonal
+ * as in PAPER.md:83-99, by the robust blocked back-substitution of Algorithm 1
+ * with augmented matrices and int32 power-of-two scaling exponents
+ * (PAPER.md:202-268).  All matrices are FP64, column-major (LAPACK convention).
+ *
+ * Conventions (those of LAPACK xTGEVC, verified as a black box in
+ * tests/test_oracle_vectors.py):
+ *  - a real eigenvalue gives one column; a complex pair gives two columns [Re z, Im z] of
+ *    the eigenvector z for the eigenvalue with positive imaginary part;
+ *  - columns are normalised so that max_i |x_i| = 1 (real) or max_i (|x_i| + |y_i|) = 1
+ *    (pair); rows below the eigenvalue's diagonal block are exactly 0;
+ *  - an indefinite 1x1 block (alpha = beta = 0) gives the unit vector e_j.
+ *
+ * Status codes (int return value, LAPACK INFO style):
+ *     0   success
+ *    -i   argument i of zz_tgevc / zz_tgevc_host is invalid (1-based)
+ *    +j   the 2x2 diagonal block S(j:j+1, j:j+1) (1-based) has real eigenvalues
+ *         (assumption 2 of PAPER.md:69 violated); X is not written
+ *  -100   CUDA error      -102 out of device memory      -103 no context (zz_init missing)
+ *  -104   non-finite entry in a diagonal block of S or T
+ *  -105   overlapping 2x2 blocks (two consecutive nonzero subdiagonal entries of S)
+ *  -106   unsupported tile size
+ * There is no CPU fallback: without a CUDA device every call returns -100 or -103.
+ *
+ * Threading.  One context per host thread (thread-local), bound to one device.  Calls on
+ * a context are not reentrant.  Multi-GPU use (one process per GPU) shards eigenvector
+ * column blocks through `select` (see paper_2003_04776_b200/dist.py); no call of this
+ * library communicates between devices.
+ */
+#ifndef ZZ_H
+#define ZZ_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZZ_OK 0
+#define ZZ_ERR_CUDA (-100)
+#define ZZ_ERR_NOMEM (-102)
+#define ZZ_ERR_NOCTX (-103)
+#define ZZ_ERR_NONFINITE (-104)
+#define ZZ_ERR_OVERLAP (-105)
+#define ZZ_ERR_TILE (-106)
+
+/* Statistics of the last zz_tgevc call of this thread's context. */
+typedef struct zz_info {
+  int m;              /* order of the pencil */
+  int n_sel;          /* number of output columns */
+  int mb;             /* tile size used */
+  int n_tiles;        /* M, number of tile rows (steps of the wavefront) */
+  int n_scaled;       /* columns with col_scale_exp < 0 */
+  int min_exp;        /* min col_scale_exp (0 if none scaled) */
+  int n_indefinite;   /* indefinite eigenvalues among the selected ones */
+  int prescaled;      /* 1 if S or T was pre-scaled by a power of two (reading R6) */
+  int update_launches;     /* robust-update kernel launches */
+  int total_launches;      /* all kernel launches of the call */
+  double ms_setup;         /* structure scan, pairs, norms */
+  double ms_steps;         /* the wavefront (diagonal solves + updates) */
+  double ms_normalize;     /* consistency and normalisation */
+  double ms_update;        /* summed device time of the robust-update kernels (if timed) */
+} zz_info_t;
+
+/* Create (or re-bind) this thread's context on CUDA device `device`.
+ * Returns 0 or -100 (no such device / CUDA error). */
+int zz_init(int device);
+
+/* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = legacy default
+ * stream).  The stream is borrowed, never destroyed.  Returns 0 or -103. */
+int zz_set_stream(void* stream);
+
+/* Tile size mb (rows of the diagonal tiles): 0 = automatic (128), or a
+ * multiple of 16 in [32, 160].  A tile boundary that would split a 2x2 block moves up one
+ * row (reading R12).  Returns 0, -103 or -106. */
+int zz_set_tile(int mb);
+
+/* Per-kernel timing of the robust update with CUDA events (0 off, 1 on): fills
+ * zz_info_t.ms_update.  Adds an event pair per step; used by bench.py for the roofline. */
+int zz_set_timing(int on);
+
+/*
+ * zz_tgevc: selected right eigenvectors on the device.
+ *   m              order of S and T (m >= 0)                                   [arg 1]
+ *   S, lds         DEVICE, m x m column-major, lds >= max(1,m); never written  [args 2,3]
+ *   T, ldt         DEVICE, m x m column-major, ldt >= max(1,m); never written  [args 4,5]
+ *   select         HOST int[m] or NULL (all eigenvectors).  select[j] != 0 picks
+ *                  eigenvalue j; a complex pair (j, j+1) is computed if either flag is
+ *                  set.  Output columns are packed in block order.           [arg 6]
+ *   X, ldx         DEVICE, m x n_sel column-major, ldx >= max(1,m); written
+ *                  completely (including the zeros below each column's block)  [args 7,8]
+ *   col_scale_exp  DEVICE int32[n_sel] or NULL: e_c <= 0 such that the tip-normalised
+ *                  eigenvector (x_r = 1) is 2^-e_c times the column before
+ *                  normalisation (Definition 1).  Both columns of a
+ *                  pair carry the same e_c.  Values are implementation-defined.  [arg 9]
+ * The strictly lower parts of S (outside the 2x2 blocks) and of T are never read.
+ * Work runs on the context's stream; the call returns after the stream has completed.
+ * Ownership: S, T, X, col_scale_exp are caller-owned; the library owns a workspace grown
+ * on demand and freed by zz_finalize.
+ */
+int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+             double* X, int ldx, int* col_scale_exp);
+
+/* zz_tgevc_host: the same operation with HOST S, T, X, col_scale_exp (pinned memory
+ * recommended).  The library stages S and T into device memory, solves, and copies X and
+ * col_scale_exp back, all on the context's stream (end-to-end path of bench.py).
+ * Arguments and status codes as zz_tgevc. */
+int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+                  double* X, int ldx, int* col_scale_exp);
+
+/* Number of output columns zz_tgevc would produce for (S, select) with S on the HOST
+ * (pairs count 2).  Returns n_sel >= 0, -105, or -i for a bad argument.  Host-only. */
+int zz_count_columns(int m, const double* S_host, int lds, const int* select);
+
+/* Host-only tile partition (reading R12): given the m-1
+ * subdiagonal entries sub[j] = S(j+1,j) (HOST) and mb, writes tile_start[0..M] (M+1
+ * entries, tile_start[M] = m) and returns M, or -105 / -106.  tile_start must hold
+ * m/(mb-1)+2 ints. */
+int zz_partition(int m, const double* sub, int mb, int* tile_start);
+
+/* Statistics of the last call.  Returns 0 or -103. */
+int zz_last_info(zz_info_t* out);
+
+/* Free the workspace and the context of this thread.  Returns 0. */
+int zz_finalize(void);
+
+/* Static description of a status code. */
+const char* zz_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZZ_H */

@@ -1,0 +1,285 @@
+"""paper_2003_04776_b200 -- B200-native robust generalized eigenvectors of a real Schur pencil.
+
+Thin ctypes binding of the C ABI in include/zz.h (argument marshalling only; every step of
+the computation runs in the CUDA kernels of csrc/).  PyTorch is used for device memory and
+streams.  There is no CPU fallback: without the built library or a CUDA device every call
+raises.
+
+Method: Kjelgaard Mikkelsen & Myllykoski, "Parallel Robust Computation of Generalized
+Eigenvectors of Matrix Pencils": solve S V D - T V B = 0 by the
+robust blocked back-substitution of Algorithm 1 with augmented matrices
+and int32 power-of-two scaling exponents.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libzz.so")
+_lib = None
+
+STATUS = {
+    0: "success",
+    -100: "CUDA error",
+    -102: "out of device memory",
+    -103: "no context",
+    -104: "non-finite entry in a diagonal block",
+    -105: "overlapping 2x2 blocks",
+    -106: "unsupported tile size",
+}
+
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host",
+           "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
+
+
+class ZZError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        msg = STATUS.get(status, "2x2 block with real eigenvalues at row %d" % status if status > 0
+                         else "invalid argument %d" % -status)
+        super().__init__("%s: status %d (%s)" % (what or "zz", status, msg))
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int), ("n_sel", ctypes.c_int), ("mb", ctypes.c_int),
+                ("n_tiles", ctypes.c_int), ("n_scaled", ctypes.c_int), ("min_exp", ctypes.c_int),
+                ("n_indefinite", ctypes.c_int), ("prescaled", ctypes.c_int),
+                ("update_launches", ctypes.c_int), ("total_launches", ctypes.c_int),
+                ("ms_setup", ctypes.c_double), ("ms_steps", ctypes.c_double),
+                ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def library_path():
+    return _SO
+
+
+def load(build_if_missing=True):
+    """Load libzz.so (building it in-tree with nvcc if missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        from . import _build
+        try:
+            _build.build()
+        except Exception:
+            if not os.path.exists(_SO):
+                raise
+    if not os.path.exists(_SO):
+        raise ImportError("paper_2003_04776_b200: CUDA library %s is missing (run __graft_entry__.build())" % _SO)
+    lib = ctypes.CDLL(_SO)
+    vp, ci = ctypes.c_void_p, ctypes.c_int
+    sig = {
+        "zz_init": ([ci], ci),
+        "zz_set_stream": ([vp], ci),
+        "zz_set_tile": ([ci], ci),
+        "zz_set_timing": ([ci], ci),
+        "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
+        "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
+        "zz_count_columns": ([ci, vp, ci, vp], ci),
+        "zz_partition": ([ci, vp, ci, vp], ci),
+        "zz_last_info": ([ctypes.POINTER(Info)], ci),
+        "zz_finalize": ([], ci),
+        "zz_status_string": ([ci], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(st, what):
+    if st != 0:
+        raise ZZError(st, what)
+
+
+_inited = {}
+
+
+def init(device=None):
+    """Create this thread's context on `device` (default: torch's current device)."""
+    import torch
+    if device is None:
+        device = torch.cuda.current_device()
+    lib = load()
+    _check(lib.zz_init(int(device)), "zz_init")
+    _inited[device] = True
+    return device
+
+
+def set_tile(mb):
+    _check(load().zz_set_tile(int(mb)), "zz_set_tile")
+
+
+def set_timing(on):
+    _check(load().zz_set_timing(1 if on else 0), "zz_set_timing")
+
+
+def last_info():
+    inf = Info()
+    _check(load().zz_last_info(ctypes.byref(inf)), "zz_last_info")
+    return inf.as_dict()
+
+
+def _ld_colmajor(A, m, what):
+    """leading dimension of a column-major 2-D tensor/array (stride(0) == 1)"""
+    if A.dim() != 2 if hasattr(A, "dim") else A.ndim != 2:
+        raise ValueError("%s must be 2-D" % what)
+    st = A.stride() if hasattr(A, "stride") and callable(A.stride) else tuple(s // 8 for s in A.strides)
+    if A.shape[0] != m:
+        raise ValueError("%s must have %d rows" % (what, m))
+    if A.shape[1] > 1 and st[0] != 1:
+        raise ValueError("%s must be column-major (stride(0) == 1); use colmajor()" % what)
+    return max(st[1] if A.shape[1] > 1 else m, 1)
+
+
+def colmajor(A):
+    """Column-major copy/view of a 2-D torch tensor (element (i,j) at i + j*ld)."""
+    return A.t().contiguous().t()
+
+
+def empty_colmajor(m, n, device="cuda", dtype=None, pin_memory=False):
+    import torch
+    dtype = dtype or torch.float64
+    if device == "cpu":
+        return torch.empty((n, m), dtype=dtype, pin_memory=pin_memory).t()
+    return torch.empty((n, m), dtype=dtype, device=device).t()
+
+
+def _sel_array(select, m):
+    if select is None:
+        return None
+    import numpy as np
+    s = np.ascontiguousarray(np.asarray(select.cpu() if hasattr(select, "cpu") else select, dtype=np.int32))
+    if s.size != m:
+        raise ValueError("select must have m entries")
+    return s
+
+
+def count_columns(S_host, select=None):
+    """Number of output columns for (S, select); S on the host (numpy, column-major)."""
+    import numpy as np
+    S_host = np.asfortranarray(S_host, dtype=np.float64)
+    m = S_host.shape[0]
+    sel = _sel_array(select, m)
+    n = load().zz_count_columns(m, S_host.ctypes.data, max(m, 1), None if sel is None else sel.ctypes.data)
+    if n < 0:
+        raise ZZError(n, "zz_count_columns")
+    return n
+
+
+def partition(sub, m, mb):
+    """Host tile partition (reading R12): returns tile_start[0..M]."""
+    import numpy as np
+    s = np.ascontiguousarray(np.asarray(sub, dtype=np.float64).reshape(-1))
+    out = np.zeros(m // max(mb - 1, 1) + 3, dtype=np.int32)
+    M = load().zz_partition(m, s.ctypes.data if s.size else None, mb, out.ctypes.data)
+    if M < 0:
+        raise ZZError(M, "zz_partition")
+    return out[:M + 1].copy()
+
+
+def tgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None, n_sel=None):
+    """Selected right eigenvectors of the Schur pencil (S, T) on the GPU.
+
+    S, T: CUDA float64 tensors, m x m, column-major (stride(0) == 1); never written.
+    select: host int array of length m or None.  Returns (X, col_scale_exp): X is an
+    m x n_sel column-major CUDA tensor, col_scale_exp int32 (implementation-defined
+    exponents, include/zz.h)."""
+    import torch
+    lib = load()
+    m = S.shape[0]
+    if not (S.is_cuda and T.is_cuda):
+        raise ValueError("S and T must be CUDA tensors (no CPU fallback)")
+    if S.dtype != torch.float64 or T.dtype != torch.float64:
+        raise ValueError("S and T must be float64")
+    dev = S.device.index
+    if dev not in _inited:
+        init(dev)
+    lds = _ld_colmajor(S, m, "S")
+    ldt = _ld_colmajor(T, m, "T")
+    sel = _sel_array(select, m)
+    if n_sel is None:
+        if sel is None:
+            n_sel = m
+        else:
+            # count on the host from the subdiagonal
+            sub = torch.diagonal(S, -1).cpu().numpy() if m > 1 else []
+            n_sel = _count_from_sub(sub, m, sel)
+    if X is None:
+        X = empty_colmajor(m, max(n_sel, 1), device=S.device)[:, :n_sel]
+    ldx = _ld_colmajor(X, m, "X") if n_sel > 0 else max(m, 1)
+    if col_scale_exp is None:
+        col_scale_exp = torch.empty(max(n_sel, 1), dtype=torch.int32, device=S.device)[:n_sel]
+    st = stream if stream is not None else torch.cuda.current_stream(S.device)
+    _check(lib.zz_set_stream(ctypes.c_void_p(st.cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc(m, S.data_ptr(), lds, T.data_ptr(), ldt, None if sel is None else sel.ctypes.data,
+                     X.data_ptr() if n_sel > 0 else ctypes.c_void_p(1), ldx,
+                     col_scale_exp.data_ptr() if n_sel > 0 else None)
+    _check(r, "zz_tgevc")
+    return X, col_scale_exp
+
+
+def _count_from_sub(sub, m, sel):
+    n, j = 0, 0
+    while j < m:
+        two = j + 1 < m and sub[j] != 0.0
+        sz = 2 if two else 1
+        if sel is None or sel[j] or (two and sel[j + 1]):
+            n += sz
+        j += sz
+    return n
+
+
+def tgevc_host(S, T, select=None, X=None, col_scale_exp=None, device=None):
+    """End-to-end variant: HOST S, T (column-major numpy arrays or CPU tensors, pinned memory
+    recommended); returns host X (m x n_sel) and col_scale_exp.  Staging copies are part of
+    the call (zz_tgevc_host)."""
+    import numpy as np
+    lib = load()
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    if device not in _inited:
+        init(device)
+    m = S.shape[0]
+
+    def ptr_ld(A, what):
+        if hasattr(A, "data_ptr"):
+            return A.data_ptr(), _ld_colmajor(A, m, what)
+        A = np.asarray(A)
+        if not A.flags.f_contiguous or A.dtype != np.float64:
+            raise ValueError("%s must be a Fortran-ordered float64 array" % what)
+        return A.ctypes.data, max(m, 1)
+
+    sel = _sel_array(select, m)
+    ps, lds = ptr_ld(S, "S")
+    pt, ldt = ptr_ld(T, "T")
+    if X is None:
+        if hasattr(S, "data_ptr"):
+            sub = np.diagonal(S.numpy(), -1) if m > 1 else []
+        else:
+            sub = np.diagonal(S, -1) if m > 1 else []
+        n = _count_from_sub(sub, m, sel)
+        X = np.zeros((m, max(n, 1)), order="F")[:, :n]
+    n = X.shape[1]
+    px, ldx = ptr_ld(X, "X") if n > 0 else (X.ctypes.data if hasattr(X, "ctypes") else X.data_ptr(), max(m, 1))
+    if col_scale_exp is None:
+        col_scale_exp = np.zeros(max(n, 1), np.int32)[:n]
+    pe = col_scale_exp.ctypes.data if hasattr(col_scale_exp, "ctypes") else col_scale_exp.data_ptr()
+    import torch
+    _check(lib.zz_set_stream(ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc_host(m, ps, lds, pt, ldt, None if sel is None else sel.ctypes.data, px, ldx,
+                          pe if n > 0 else None)
+    _check(r, "zz_tgevc_host")
+    return X, col_scale_exp
+
+
+def finalize():
+    if _lib is not None:
+        _lib.zz_finalize()
+    _inited.clear()

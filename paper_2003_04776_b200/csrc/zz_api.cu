@@ -1,0 +1,586 @@
+// zz_api.cu -- host runtime and C ABI (include/zz.h) of the B200 robust eigenvector path.
+//
+// The runtime owns a per-thread context (device, stream, tile size, workspace), builds the
+// plan of one call on the host (block structure, tile partition, selection, column and
+// item maps -- PAPER.md:128-132, 268-273), and drives the bottom-up wavefront over tile
+// rows (Algorithm 1): for I = M-1..0, the robust diagonal solve of tile
+// row I for every active eigenvector (tips for the blocks inside tile I), then one fused
+// robust update of all rows above it.  Two host synchronisations happen before the
+// wavefront (structure, then pair/norm status); none inside it.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/zz.h"
+#include "zz_internal.cuh"
+
+using namespace zz;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) { p = nullptr; return e; }
+    cap = want;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct Context {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int mb = 0;
+  int timing = 0;
+  zz_info_t info;
+  EncodeTiledFn encode = nullptr;
+  // workspace
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc;
+  Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  ~Context() {}
+  void release() {
+    Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
+                  &status, &tmp, &Sc, &Tc, &hS, &hT, &hX, &hE};
+    for (Buf* b : all) b->release();
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+    if (e0) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); }
+    e0 = e1 = e2 = e3 = nullptr;
+  }
+};
+
+thread_local Context* g_ctx = nullptr;
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t _e = (x);                       \
+    if (_e != cudaSuccess) return map_err(_e);  \
+  } while (0)
+
+int map_err(cudaError_t e) {
+  if (e == cudaErrorMemoryAllocation) return ZZ_ERR_NOMEM;
+  return ZZ_ERR_CUDA;
+}
+
+int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Tile partition (reading R12): nominal boundaries every mb
+// rows; a boundary that would split a 2x2 block (i.e. fall on the block's second row)
+// moves up one row, so that every tile has at most mb rows.
+int partition_host(int m, const std::vector<char>& two_bot, int mb, std::vector<int>& ts) {
+  ts.clear();
+  ts.push_back(0);
+  int s = 0;
+  while (s < m) {
+    int nx = s + mb;
+    if (nx >= m) { nx = m; }
+    else if (two_bot[nx]) nx -= 1;
+    ts.push_back(nx);
+    s = nx;
+  }
+  return (int)ts.size() - 1;
+}
+
+// blocks from the subdiagonal: returns nb or -105
+int blocks_host(int m, const double* sub, std::vector<int>& bs, std::vector<int>& bz) {
+  bs.clear();
+  bz.clear();
+  int j = 0;
+  while (j < m) {
+    bool two = (j + 1 < m) && sub[j] != 0.0;
+    if (two && j + 2 < m && sub[j + 1] != 0.0) return ZZ_ERR_OVERLAP;
+    bs.push_back(j);
+    bz.push_back(two ? 2 : 1);
+    j += two ? 2 : 1;
+  }
+  return (int)bs.size();
+}
+
+int tile_of(int mb_user) { return mb_user > 0 ? mb_user : 128; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int make_map(Context* c, CUtensorMap* tm, const double* A, long long lda, int m) {
+  if (!c->encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return ZZ_ERR_CUDA;
+    c->encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)m};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
+  cuuint32_t box[2] = {8, (cuuint32_t)kBK};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : ZZ_ERR_CUDA;
+}
+
+// The solve on device pointers.  S/T are const; X, cse written.
+int tgevc_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
+                 const int* select, double* X, long long ldx, int* cse) {
+  cudaStream_t st = c->stream;
+  zz_info_t info;
+  memset(&info, 0, sizeof(info));
+  info.m = m;
+  const int mb = tile_of(c->mb);
+  info.mb = mb;
+  if (!c->e0) {
+    cudaEventCreate(&c->e0); cudaEventCreate(&c->e1); cudaEventCreate(&c->e2); cudaEventCreate(&c->e3);
+  }
+  CK(cudaEventRecord(c->e0, st));
+  int launches = 0;
+  // ---- a1: structure scan (one host sync) ----
+  CK(c->sub.ensure(sizeof(double) * (size_t)std::max(m, 1)));
+  CK(launch_subdiag(S, lds, m, c->sub.as<double>(), st));
+  launches += (m > 1);
+  std::vector<double> sub((size_t)std::max(m - 1, 1), 0.0);
+  if (m > 1) CK(cudaMemcpyAsync(sub.data(), c->sub.p, sizeof(double) * (m - 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int> bs, bz;
+  int nb = blocks_host(m, sub.data(), bs, bz);
+  if (nb < 0) return nb;
+  std::vector<char> two_bot((size_t)m + 1, 0);
+  std::vector<signed char> row_flag((size_t)m, kRow1x1);
+  for (int p = 0; p < nb; ++p)
+    if (bz[p] == 2) {
+      two_bot[bs[p] + 1] = 1;
+      row_flag[bs[p]] = kRowTop2;
+      row_flag[bs[p] + 1] = kRowBot2;
+    }
+  std::vector<int> ts;
+  const int M = partition_host(m, two_bot, mb, ts);
+  info.n_tiles = M;
+  std::vector<int> row_tile((size_t)m);
+  for (int I = 0; I < M; ++I)
+    for (int i = ts[I]; i < ts[I + 1]; ++i) row_tile[i] = I;
+  // selection, packed columns, items (xTGEVC HOWMNY='S')
+  std::vector<int> blk_col((size_t)nb, -1), item_col, item_tile;
+  std::vector<int> col_r, col_tile;
+  int n_sel = 0;
+  for (int p = 0; p < nb; ++p) {
+    int j = bs[p];
+    bool sel = !select || select[j] || (bz[p] == 2 && select[j + 1]);
+    if (!sel) continue;
+    blk_col[p] = n_sel;
+    item_col.push_back(n_sel);
+    item_tile.push_back(row_tile[j]);
+    for (int q = 0; q < bz[p]; ++q) {
+      col_r.push_back(j + bz[p] - 1);
+      col_tile.push_back(row_tile[j]);
+    }
+    n_sel += bz[p];
+  }
+  info.n_sel = n_sel;
+  const int n_items = (int)item_col.size();
+  std::vector<int> tile_item((size_t)M + 1, n_items), cs((size_t)M + 1, n_sel);
+  for (int I = M - 1; I >= 0; --I) {
+    int t = tile_item[I + 1];
+    while (t > 0 && item_tile[t - 1] >= I) --t;
+    tile_item[I] = t;
+    cs[I] = (t < n_items) ? item_col[t] : n_sel;
+  }
+  // ---- workspace ----
+  const int n = std::max(n_sel, 1);
+  const int nks_max = ceil_div(mb, kBK);
+  const int n_ntiles_all = ceil_div(n, kBN);
+  CK(c->colf.ensure(sizeof(double) * 3 * (size_t)n));
+  CK(c->coli.ensure(sizeof(int) * 7 * (size_t)n));
+  CK(c->items.ensure(sizeof(int) * (size_t)std::max(n_items, 1)));
+  CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
+  CK(c->rows.ensure((sizeof(int) + 1) * (size_t)m + 16));
+  CK(c->blks.ensure(sizeof(int) * 3 * (size_t)nb));
+  CK(c->state.ensure(sizeof(unsigned long long) * 2 * (size_t)n));
+  CK(c->seg.ensure((sizeof(int) + 2 * sizeof(double)) * (size_t)M * n));
+  CK(c->norms.ensure(sizeof(double) * 4 * (size_t)M));
+  CK(c->W.ensure(sizeof(double) * (size_t)n_ntiles_all * 2 * nks_max * kBN * kBK));
+  CK(c->status.ensure(sizeof(int) * 16 + sizeof(unsigned long long) * 2));
+  CK(c->tmp.ensure((sizeof(int) + sizeof(double)) * (size_t)n + 16));
+  DevPlan P;
+  P.col_a = c->colf.as<double>();
+  P.col_b = P.col_a + n;
+  P.col_beta = P.col_b + n;
+  P.col_kind = c->coli.as<int>();
+  P.col_r = P.col_kind + n;
+  P.col_tile = P.col_r + n;
+  P.e_pend = P.col_tile + n;
+  P.sY = P.e_pend + n;
+  P.item_col = c->items.as<int>();
+  P.tile_start = c->tiles.as<int>();
+  P.row_tile = c->rows.as<int>();
+  P.row_flag = reinterpret_cast<signed char*>(P.row_tile + m);
+  P.blk_start = c->blks.as<int>();
+  P.blk_size = P.blk_start + nb;
+  P.blk_col = P.blk_size + nb;
+  P.nY = c->state.as<unsigned long long>();
+  {
+    // e_seg (int) first, then the two double arrays at an 8-byte aligned offset
+    size_t off = (sizeof(int) * (size_t)M * n + 7) / 8 * 8;
+    P.e_seg = c->seg.as<int>();
+    P.nrm_seg = reinterpret_cast<double*>(c->seg.as<char>() + off);
+  }
+  P.nrmh_seg = P.nrm_seg + (size_t)M * n;
+  P.cS = c->norms.as<double>();
+  P.cT = P.cS + M;
+  P.W = c->W.as<double>();
+  P.status = c->status.as<int>();
+  P.maxabs = reinterpret_cast<unsigned long long*>(P.status + 16);
+  int* exp_tmp = c->tmp.as<int>();
+  double* rec_tmp = reinterpret_cast<double*>(c->tmp.as<char>() + ((sizeof(int) * (size_t)n + 15) / 16 * 16));
+  // ---- upload the plan ----
+  if (n_sel > 0) {
+    CK(cudaMemcpyAsync(P.col_r, col_r.data(), sizeof(int) * n_sel, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(P.col_tile, col_tile.data(), sizeof(int) * n_sel, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(P.item_col, item_col.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(P.tile_start, ts.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P.row_tile, row_tile.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P.row_flag, row_flag.data(), m, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P.blk_start, bs.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P.blk_size, bz.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P.blk_col, blk_col.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  {
+    int init[16] = {0x7fffffff, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(P.status, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  }
+  // TMA needs 16-byte aligned bases and even leading dimensions; otherwise repack
+  const double* Su = S;
+  const double* Tu = T;
+  long long ldsu = lds, ldtu = ldt;
+  auto repack = [&](Buf& b, const double* A, long long lda, int k, const double*& out, long long& ldo) -> int {
+    long long ld2 = (m + 1) / 2 * 2;
+    cudaError_t e = b.ensure(sizeof(double) * (size_t)ld2 * m);
+    if (e != cudaSuccess) return map_err(e);
+    e = launch_scale_copy(A, lda, m, k, b.as<double>(), ld2, st);
+    if (e != cudaSuccess) return map_err(e);
+    out = b.as<double>();
+    ldo = ld2;
+    launches++;
+    return 0;
+  };
+  if ((lds & 1) || !aligned16(S)) { int r = repack(c->Sc, S, lds, 0, Su, ldsu); if (r) return r; }
+  if ((ldt & 1) || !aligned16(T)) { int r = repack(c->Tc, T, ldt, 0, Tu, ldtu); if (r) return r; }
+  // ---- a2 pairs, a3 norms (second host sync: status + pre-scale test) ----
+  for (int pass = 0; pass < 2; ++pass) {
+    CK(cudaMemsetAsync(P.cS, 0, sizeof(double) * 4 * M, st));
+    CK(launch_pairs(Su, ldsu, Tu, ldtu, nb, P, st));
+    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st));
+    launches += 2 + (M > 1);
+    std::vector<double> nrm(4 * (size_t)M);
+    int stat[16];
+    CK(cudaMemcpyAsync(stat, P.status, sizeof(stat), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(nrm.data(), P.cS, sizeof(double) * 4 * M, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (stat[0] != 0x7fffffff) {
+      int p = stat[0] >> 2, kind = stat[0] & 3;
+      return kind == 1 ? ZZ_ERR_NONFINITE : bs[p] + 1;
+    }
+    info.n_indefinite = stat[2];
+    if (pass == 1) break;
+    // pre-scale test (reading R6): every row sum of |S| is <= sum_J cS[J] + max_J dS[J]
+    double bS = 0, bT = 0, mdS = 0, mdT = 0;
+    for (int I = 0; I < M; ++I) {
+      bS += nrm[I]; bT += nrm[M + I];
+      mdS = std::max(mdS, nrm[2 * M + I]); mdT = std::max(mdT, nrm[3 * M + I]);
+    }
+    bS += mdS;
+    bT += mdT;
+    const double lim = 0x1p1020;  // Omega / 8
+    if (bS <= lim && bT <= lim) break;
+    // rare path: scale S and/or T by 2^-k (exact), so that m * maxabs <= Omega / 8
+    CK(cudaMemsetAsync(P.maxabs, 0, 16, st));
+    CK(launch_maxabs(Su, ldsu, Tu, ldtu, m, P.maxabs, st));
+    unsigned long long mx[2];
+    CK(cudaMemcpyAsync(mx, P.maxabs, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int w = 0; w < 2; ++w) {
+      double bound = w ? bT : bS;
+      if (bound <= lim) continue;
+      double amax;
+      memcpy(&amax, &mx[w], 8);
+      int ea;
+      frexp(amax, &ea);  // amax < 2^ea
+      int em = (int)ceil(log2((double)std::max(m, 2)));
+      int k = ea + em - 1020 + 1;
+      if (k < 0) k = 0;
+      int r = w ? repack(c->Tc, Tu, ldtu, k, Tu, ldtu) : repack(c->Sc, Su, ldsu, k, Su, ldsu);
+      if (r) return r;
+    }
+    info.prescaled = 1;
+    int init[16] = {0x7fffffff, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(P.status, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  }
+  if (n_sel == 0) {
+    c->info = info;
+    return 0;
+  }
+  CUtensorMap tmS, tmT;
+  if (M > 1) {
+    int r = make_map(c, &tmS, Su, ldsu, m);
+    if (!r) r = make_map(c, &tmT, Tu, ldtu, m);
+    if (r) return r;
+  }
+  CK(cudaMemsetAsync(P.e_pend, 0, sizeof(int) * n, st));
+  CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * 2 * n, st));
+  CK(cudaEventRecord(c->e1, st));
+  // ---- the wavefront (Algorithm 1 over tile rows, bottom-up) ----
+  const int vec = ((ldx & 1) == 0) && aligned16(X);
+  if (c->timing && (int)c->ev.size() < 2 * M) {
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    c->ev.assign(2 * (size_t)M, nullptr);
+    for (auto& e : c->ev) cudaEventCreate(&e);
+  }
+  int n_upd = 0;
+  for (int I = M - 1; I >= 0; --I) {
+    if (tile_item[I] >= n_items) continue;
+    DiagParams dp;
+    dp.I = I;
+    dp.t0 = ts[I];
+    dp.nt = ts[I + 1] - ts[I];
+    dp.item_begin = tile_item[I];
+    dp.n_items = n_items;
+    dp.tip_col_end = cs[I + 1];
+    dp.do_update = (I > 0);
+    dp.nks = ceil_div(dp.nt, kBK);
+    dp.n_sel = n_sel;
+    dp.S = Su; dp.lds = ldsu; dp.T = Tu; dp.ldt = ldtu;
+    dp.X = X; dp.ldx = ldx;
+    dp.P = P;
+    dp.nY_in = I & 1;
+    CK(launch_diag(dp, st));
+    launches++;
+    if (I > 0) {
+      UpdParams up;
+      up.rows = ts[I];
+      up.max_row = ts[I - 1];
+      up.t0 = ts[I];
+      up.nks = dp.nks;
+      up.c_begin = cs[I];
+      up.first_end = cs[I + 1];
+      up.n_sel = n_sel;
+      up.ntile0 = cs[I] / kBN;
+      up.X = X; up.ldx = ldx;
+      up.W = P.W;
+      up.sY = P.sY;
+      up.nY_out = P.nY + (size_t)(1 - (I & 1)) * n;
+      up.vec = vec;
+      int n_m = ceil_div(ts[I], kBM);
+      int n_n = ceil_div(n_sel, kBN) - up.ntile0;
+      if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));
+      CK(launch_update(&tmS, &tmT, up, n_m, n_n, st));
+      if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], st));
+      n_upd++;
+      launches++;
+    }
+  }
+  CK(cudaEventRecord(c->e2, st));
+  // ---- a7 consistency and normalisation ----
+  CK(launch_normalize(m, n_sel, M, X, ldx, cse, P, exp_tmp, rec_tmp, st));
+  launches += 2;
+  CK(cudaEventRecord(c->e3, st));
+  int stat[16];
+  CK(cudaMemcpyAsync(stat, P.status, sizeof(stat), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  info.n_scaled = stat[4];
+  info.min_exp = stat[5];
+  info.update_launches = n_upd;
+  info.total_launches = launches;
+  float ms;
+  cudaEventElapsedTime(&ms, c->e0, c->e1); info.ms_setup = ms;
+  cudaEventElapsedTime(&ms, c->e1, c->e2); info.ms_steps = ms;
+  cudaEventElapsedTime(&ms, c->e2, c->e3); info.ms_normalize = ms;
+  if (c->timing) {
+    double tot = 0;
+    for (int u = 0; u < n_upd; ++u) {
+      cudaEventElapsedTime(&ms, c->ev[2 * u], c->ev[2 * u + 1]);
+      tot += ms;
+    }
+    info.ms_update = tot;
+  }
+  c->info = info;
+  return 0;
+}
+
+int check_args(int m, const double* S, int lds, const double* T, int ldt, double* X, int ldx) {
+  if (m < 0) return -1;
+  if (m > 0 && !S) return -2;
+  if (lds < std::max(1, m)) return -3;
+  if (m > 0 && !T) return -4;
+  if (ldt < std::max(1, m)) return -5;
+  if (m > 0 && !X) return -7;
+  if (ldx < std::max(1, m)) return -8;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int zz_init(int device) {
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess || device < 0 || device >= nd) return ZZ_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (g_ctx && g_ctx->device != device) {
+    g_ctx->release();
+    delete g_ctx;
+    g_ctx = nullptr;
+  }
+  if (!g_ctx) {
+    g_ctx = new Context();
+    memset(&g_ctx->info, 0, sizeof(g_ctx->info));
+  }
+  g_ctx->device = device;
+  return 0;
+}
+
+int zz_set_stream(void* stream) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  g_ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  return 0;
+}
+
+int zz_set_tile(int mb) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (mb != 0 && (mb < 32 || mb > kMaxMB || (mb % 16) != 0)) return ZZ_ERR_TILE;
+  g_ctx->mb = mb;
+  return 0;
+}
+
+int zz_set_timing(int on) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  g_ctx->timing = on ? 1 : 0;
+  return 0;
+}
+
+int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,
+             int ldx, int* col_scale_exp) {
+  int a = check_args(m, S, lds, T, ldt, X, ldx);
+  if (a) return a;
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (cudaSetDevice(g_ctx->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (m == 0) {
+    memset(&g_ctx->info, 0, sizeof(g_ctx->info));
+    return 0;
+  }
+  return tgevc_device(g_ctx, m, S, lds, T, ldt, select, X, ldx, col_scale_exp);
+}
+
+int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,
+                  int ldx, int* col_scale_exp) {
+  int a = check_args(m, S, lds, T, ldt, X, ldx);
+  if (a) return a;
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  Context* c = g_ctx;
+  if (cudaSetDevice(c->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (m == 0) return 0;
+  int n_sel = zz_count_columns(m, S, lds, select);
+  if (n_sel < 0) return n_sel;
+  cudaStream_t st = c->stream;
+  long long ld = (m + 1) / 2 * 2;
+  CK(c->hS.ensure(sizeof(double) * (size_t)ld * m));
+  CK(c->hT.ensure(sizeof(double) * (size_t)ld * m));
+  CK(c->hX.ensure(sizeof(double) * (size_t)ld * std::max(n_sel, 1)));
+  CK(c->hE.ensure(sizeof(int) * (size_t)std::max(n_sel, 1)));
+  CK(cudaMemcpy2DAsync(c->hS.p, ld * 8, S, (size_t)lds * 8, (size_t)m * 8, m, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpy2DAsync(c->hT.p, ld * 8, T, (size_t)ldt * 8, (size_t)m * 8, m, cudaMemcpyHostToDevice, st));
+  int r = tgevc_device(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
+                       c->hE.as<int>());
+  if (r) return r;
+  if (n_sel > 0) {
+    CK(cudaMemcpy2DAsync(X, (size_t)ldx * 8, c->hX.p, ld * 8, (size_t)m * 8, n_sel, cudaMemcpyDeviceToHost, st));
+    if (col_scale_exp)
+      CK(cudaMemcpyAsync(col_scale_exp, c->hE.p, sizeof(int) * n_sel, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int zz_count_columns(int m, const double* S_host, int lds, const int* select) {
+  if (m < 0) return -1;
+  if (m > 0 && !S_host) return -2;
+  if (lds < std::max(1, m)) return -3;
+  int n = 0, j = 0;
+  while (j < m) {
+    bool two = (j + 1 < m) && S_host[(size_t)j * lds + j + 1] != 0.0;
+    if (two && j + 2 < m && S_host[(size_t)(j + 1) * lds + j + 2] != 0.0) return ZZ_ERR_OVERLAP;
+    int sz = two ? 2 : 1;
+    if (!select || select[j] || (two && select[j + 1])) n += sz;
+    j += sz;
+  }
+  return n;
+}
+
+int zz_partition(int m, const double* sub, int mb, int* tile_start) {
+  if (m < 0) return -1;
+  if (mb < 2) return ZZ_ERR_TILE;
+  std::vector<double> s((size_t)std::max(m, 1), 0.0);
+  if (m > 1) memcpy(s.data(), sub, sizeof(double) * (m - 1));
+  std::vector<int> bs, bz;
+  int nb = blocks_host(m, s.data(), bs, bz);
+  if (nb < 0) return nb;
+  std::vector<char> two_bot((size_t)m + 1, 0);
+  for (int p = 0; p < nb; ++p)
+    if (bz[p] == 2) two_bot[bs[p] + 1] = 1;
+  std::vector<int> ts;
+  int M = partition_host(m, two_bot, mb, ts);
+  for (int I = 0; I <= M; ++I) tile_start[I] = ts[I];
+  return M;
+}
+
+int zz_last_info(zz_info_t* out) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (out) *out = g_ctx->info;
+  return 0;
+}
+
+int zz_finalize(void) {
+  if (g_ctx) {
+    g_ctx->release();
+    delete g_ctx;
+    g_ctx = nullptr;
+  }
+  return 0;
+}
+
+const char* zz_status_string(int s) {
+  if (s == 0) return "success";
+  if (s > 0) return "a 2x2 diagonal block has real eigenvalues (assumption 2 violated)";
+  switch (s) {
+    case ZZ_ERR_CUDA: return "CUDA error (or no CUDA device)";
+    case ZZ_ERR_NOMEM: return "out of device memory";
+    case ZZ_ERR_NOCTX: return "no context: call zz_init first";
+    case ZZ_ERR_NONFINITE: return "non-finite entry in a diagonal block of S or T";
+    case ZZ_ERR_OVERLAP: return "overlapping 2x2 blocks (two consecutive nonzero subdiagonals)";
+    case ZZ_ERR_TILE: return "unsupported tile size";
+    default: return (s >= -9) ? "invalid argument" : "unknown status";
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// zz_internal.cuh -- internal declarations of the B200 (sm_100a) robust eigenvector path.
+// Product code: never includes or links anything under oracle/.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace zz {
+
+// ------------------------------------------------------------------------------------
+// Constants (readings R1, R8): Omega = 2^1023, u = 2^-53, smlnum = 2^-969.
+// ------------------------------------------------------------------------------------
+constexpr double kOmega = 0x1p1023;
+constexpr double kU = 0x1p-53;
+constexpr double kSmlnum = 0x1p-969;
+
+// GEMM (robust update) tiling, shared by the update kernel and the W writer of the
+// diagonal solve (W is stored in the update kernel's shared-memory stage order).
+constexpr int kBM = 128;   // rows of X per CTA tile
+constexpr int kBN = 64;    // eigenvector columns per CTA tile
+constexpr int kBK = 16;    // K chunk (columns of S or T per pipeline stage)
+constexpr int kMaxMB = 160;
+
+// column kinds
+enum : int { kReal = 0, kPairFirst = 1, kPairSecond = 2, kIndefinite = 3 };
+// row flags inside the diagonal structure
+enum : int { kRow1x1 = 0, kRowTop2 = 1, kRowBot2 = 2 };
+
+// ------------------------------------------------------------------------------------
+// Overflow protection.  Definitions of DESIGN.md R4/R5; written with
+// explicit round-to-nearest intrinsics so that no contraction changes the decision.
+// ------------------------------------------------------------------------------------
+// ProtectUpdate(y, t, x) -> e with 2^e (y + t x) <= Omega
+__device__ __forceinline__ int protect_update(double y, double t, double x) {
+  double s = __dadd_rn(__dmul_rn(y, 0x1p-1023), __dmul_rn(__dmul_rn(t, 0x1p-512), __dmul_rn(x, 0x1p-511)));
+  if (s <= 0.5) return 0;
+  int k;
+  double f = frexp(s, &k);
+  int c = (f == 0.5) ? k - 1 : k;
+  return -c - 1;
+}
+// ProtectDivision(b, t) -> e with 2^e b <= t Omega
+__device__ __forceinline__ int protect_division(double b, double t) {
+  if (t >= 1.0 || b <= __dmul_rn(t, kOmega)) return 0;
+  double r = __ddiv_rn(__dmul_rn(t, kOmega), b);
+  int k;
+  frexp(r, &k);
+  return k - 2;
+}
+
+// ------------------------------------------------------------------------------------
+// Host-side plan of one call (built by zz_api.cu, copied to the device).
+// ------------------------------------------------------------------------------------
+struct DevPlan {
+  // per output column c (n_sel)
+  double* col_a;
+  double* col_b;
+  double* col_beta;
+  int* col_kind;
+  int* col_r;         // last row of the column's diagonal block
+  int* col_tile;      // tile index of that block
+  // per item (selected block) t
+  int* item_col;      // first output column
+  // per tile
+  int* tile_start;    // M+1
+  // per row
+  signed char* row_flag;
+  int* row_tile;
+  // per block (all blocks) for the pair kernel
+  int* blk_start;
+  int* blk_size;
+  int* blk_col;       // first output column or -1
+  // robustness state
+  int* e_pend;        // per column: exponent of the pending (not yet solved) rows
+  int* sY;            // per column: exponent shift of the pending rows at this step
+  unsigned long long* nY;   // 2 x n_sel: max |pending| (double bits), double buffered
+  int* e_seg;         // M x n_sel: exponent of each solved segment
+  double* nrm_seg;    // M x n_sel: max(|Re|,|Im|) of the segment
+  double* nrmh_seg;   // M x n_sel: max(|x|/2 + |y|/2) (pair) or |x|/2 (real)
+  double* cS;         // M: infinity norm of the S panel above tile I
+  double* cT;
+  double* W;          // update B operand, blocked [ntile][kc][BK/4][BN][4]
+  int* status;        // [0]: first bad 2x2 row (1-based) or 0; [1]: nonfinite flag;
+                      // [2]: indefinite count; [3]: maxabs bits lo; ...
+  unsigned long long* maxabs;  // [0] S, [1] T (double bits)
+};
+
+struct DiagParams {
+  int I, t0, nt;
+  int item_begin, n_items;
+  int tip_col_end;   // columns < tip_col_end (and >= first active) are tips
+  int do_update;
+  int nks;           // K chunks per part (S or T) in W for this step
+  int n_sel;
+  const double* S; long long lds;
+  const double* T; long long ldt;
+  double* X; long long ldx;
+  DevPlan P;
+  int nY_in;         // which nY buffer holds the pending max of this step
+};
+
+struct UpdParams {
+  int rows;          // ts_I: rows [0, rows) are updated
+  int max_row;       // ts_{I-1}: rows [0, max_row) form the next pending region
+  int t0;            // first column of tile I in S and T
+  int nks;           // K chunks per part
+  int c_begin;       // first active column (cs_I)
+  int first_end;     // columns < first_end start from C = 0 (cs_{I+1})
+  int n_sel;
+  int ntile0;        // first N tile index (c_begin / BN)
+  double* X; long long ldx;
+  const double* W;
+  const int* sY;
+  unsigned long long* nY_out;
+  int vec;           // 16-byte aligned X access possible
+};
+
+// launchers (zz_kernels.cu / zz_update.cu)
+cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, cudaStream_t st);
+cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int nblk,
+                         const DevPlan& P, cudaStream_t st);
+cudaError_t launch_maxabs(const double* S, long long lds, const double* T, long long ldt, int m,
+                          unsigned long long* out, cudaStream_t st);
+cudaError_t launch_rowsum_max(const double* A, long long lda, int m, unsigned long long* out,
+                              cudaStream_t st);
+cudaError_t launch_scale_copy(const double* A, long long lda, int m, int k, double* B, long long ldb,
+                              cudaStream_t st);
+cudaError_t launch_panel_norms(const double* S, long long lds, const double* T, long long ldt, int M,
+                               const int* tile_start_host, const DevPlan& P, cudaStream_t st);
+cudaError_t launch_diag(const DiagParams& p, cudaStream_t st);
+cudaError_t launch_normalize(int m, int n_sel, int M, double* X, long long ldx, int* col_scale_exp,
+                             const DevPlan& P, int* exp_tmp, double* rec_tmp, cudaStream_t st);
+cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
+                          int n_mtiles, int n_ntiles, cudaStream_t st);
+size_t diag_smem_bytes(int nt);
+
+}  // namespace zz

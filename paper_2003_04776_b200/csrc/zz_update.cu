@@ -1,0 +1,221 @@
+// zz_update.cu -- the robust update (Kernel 2 of PAPER.md:153-157, Alg. 1 line P:140) as
+// one fused FP64 contraction per wavefront step I (the composition of PAPER.md:235):
+//
+//   Y[0:ts_I, c] <- 2^sY[c] Y[0:ts_I, c] + [S(0:ts_I, tile I) | T(0:ts_I, tile I)] W[:, c]
+//   W = [-2^sX X_I D ; 2^sX X_I B]    (formed by the diagonal solve, zz_kernels.cu)
+//
+// with the per-column exponents sY/sX chosen by ProtectUpdate (Algs. 2 and 3,
+// PAPER.md:216-262), and an epilogue that writes the new max|Y| per column (the norm the
+// next step's scaling decision needs).
+//
+// B200 design: FP64 has no tcgen05 kind on sm_100a; the tensor path is DMMA.8x8x4
+// (mma.sync.m8n8k4.f64), measured at 37.0 TFLOP/s = the DFMA peak (profiles/).  The CTA
+// tile is 128 rows x 64 columns, K is consumed in chunks of 16 through a 4-stage
+// TMA / bulk-copy pipeline with mbarriers; one producer warp, four DMMA warps (64 x 32
+// each).  The contraction is computed transposed (C^T = W^T S^T) so that each lane's two
+// accumulators are two consecutive rows of a column of X: 16-byte loads/stores of C.
+#include <cuda.h>
+#include <stdint.h>
+
+#include "zz_internal.cuh"
+
+namespace zz {
+
+constexpr int kStages = 4;
+constexpr int kCWarps = 4;                 // DMMA (consumer) warps
+constexpr int kThreads = (kCWarps + 1) * 32;
+constexpr int kABytes = kBM * kBK * 8;     // S or T chunk: [BM/8][BK][8] doubles
+constexpr int kBBytes = kBN * kBK * 8;     // W chunk:      [BK/4][BN][4] doubles
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kBN * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kCWarps * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    k_update(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntile = p.ntile0 + blockIdx.x;
+  const int n0 = ntile * kBN, m0 = blockIdx.y * kBM;
+  const int nkc = 2 * p.nks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < kBN) colmax[threadIdx.x] = 0ull;
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------- producer: TMA (S/T chunks) + bulk copy (W chunk) ----------------
+    if (lane == 0) {
+      const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int s = kc % kStages;
+        if (kc >= kStages) mbar_wait(&empty[s], ((kc / kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kStageBytes);
+        const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
+        const int kcol = p.t0 + (kc % p.nks) * kBK;
+        double* a = sA + s * (kBM * kBK);
+#pragma unroll 4
+        for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
+        bulk_load(sB + s * (kBN * kBK), wt + (long long)kc * (kBN * kBK), kBBytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: 4 warps, 2 (rows) x 2 (columns), 64 x 32 each ----------------
+  const int wm = warp >> 1, wn = warp & 1;
+  const int rq = lane & 3, cq = lane >> 2;
+  double acc[4][8][2];
+  // accumulators start from the scaled pending values: 2^sY[c] * Y (exact)
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+    const int c = n0 + wn * 32 + ni * 8 + cq;
+    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
+    const bool ld = cvalid && (c >= p.first_end);
+    const int sy = ld ? p.sY[c] : 0;
+    const double* xc = p.X + (long long)c * p.ldx;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      double v0 = 0.0, v1 = 0.0;
+      if (ld && i0 < p.rows) {
+        if (p.vec && i0 + 1 < p.rows) {
+          double2 t = *reinterpret_cast<const double2*>(xc + i0);
+          v0 = t.x; v1 = t.y;
+        } else {
+          v0 = xc[i0];
+          if (i0 + 1 < p.rows) v1 = xc[i0 + 1];
+        }
+        if (sy != 0) { v0 = ldexp(v0, sy); v1 = ldexp(v1, sy); }
+      }
+      acc[ni][mi][0] = v0;
+      acc[ni][mi][1] = v1;
+    }
+  }
+
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int s = kc % kStages;
+    mbar_wait(&full[s], (kc / kStages) & 1);
+    const double* a = sA + s * (kBM * kBK);
+    const double* b = sB + s * (kBN * kBK);
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      double fw[4], fs[8];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wn * 32 + ni * 8 + cq) * 4 + rq];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+    const int c = n0 + wn * 32 + ni * 8 + cq;
+    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
+    double* xc = p.X + (long long)c * p.ldx;
+    double cm = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
+      if (cvalid && i0 < p.rows) {
+        if (p.vec && i0 + 1 < p.rows) {
+          *reinterpret_cast<double2*>(xc + i0) = make_double2(v0, v1);
+        } else {
+          xc[i0] = v0;
+          if (i0 + 1 < p.rows) xc[i0 + 1] = v1;
+        }
+      }
+      if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
+      if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
+    }
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+    if (rq == 0 && cvalid && cm > 0.0)
+      atomicMax(&colmax[c - n0], (unsigned long long)__double_as_longlong(cm));
+  }
+  consumer_sync();
+  if (threadIdx.x < kBN) {
+    const int c = n0 + threadIdx.x;
+    const unsigned long long v = colmax[threadIdx.x];
+    if (v != 0ull && c >= p.c_begin && c < p.n_sel) atomicMax(&p.nY_out[c], v);
+  }
+}
+
+cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
+                          int n_mtiles, int n_ntiles, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
+  dim3 grid(n_ntiles, n_mtiles);
+  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
+  return cudaGetLastError();
+}
+
+}  // namespace zz
