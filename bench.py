@@ -1,0 +1,368 @@
+"""bench.py -- time-to-solution and FP64 TFLOP/s of the robust generalized-eigenvector path.
+
+Metric (BASELINE.json): "seconds & FP64 TFLOP/s, all eigenvectors, m=40000, at 1/2/4/8
+B200".  A step is one call of the public API computing all m eigenvectors of the seeded
+synthetic C4 pencil (m = 40000); value = F / t with the nominal work
+F = sum_c 2 r_c (r_c - 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C4] [--mb 128] [--no-e2e] [--no-cpu]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL): S and T are broadcast from rank 0,
+column blocks are sharded cyclically, X is gathered on rank 0 (all inside the timed
+region); the time is the max over ranks.  `--impl reference` times the oracle (the
+plain CPU implementation, oracle/) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "seconds & FP64 TFLOP/s, all eigenvectors, m=40000, at 1/2/4/8 B200"
+FP64_PEAK = 37.0   # TFLOP/s, measured DMMA.8x8x4 loop on this pool (profiles/r01_fp64_peak.json)
+PEAK_SRC = ("measured: DMMA.8x8x4 / DFMA register loops 37.0 / 37.1 TFLOP/s at 1965 MHz, cuBLAS "
+            "DGEMM 35.5 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry "
+            "(its bf16 1650.8 x the guide's nominal FP64:BF16 45:2250 would give 33.0)")
+
+
+def blocks_from_sub(sub, m):
+    out, j = [], 0
+    while j < m:
+        two = j + 1 < m and sub[j] != 0.0
+        out.append((j, 2 if two else 1))
+        j += 2 if two else 1
+    return out
+
+
+def nominal_flops(blocks, select=None):
+    """F(select) = sum over selected columns of 2 r (r - 1), r = 1-based last row."""
+    f = 0.0
+    for j, sz in blocks:
+        if select is None or select[j] or (sz == 2 and select[j + 1]):
+            r = float(j + sz)
+            f += sz * 2.0 * r * (r - 1.0)
+    return f
+
+
+def update_flops(blocks, m, mb):
+    """Algorithmic flops of all robust-update launches (4 per (row above tile I, column,
+    row of tile I inside the column's support)) and per-launch list."""
+    two_bot = np.zeros(m + 1, bool)
+    for j, sz in blocks:
+        if sz == 2:
+            two_bot[j + 1] = True
+    ts = [0]
+    while ts[-1] < m:
+        nx = ts[-1] + mb
+        if nx >= m:
+            nx = m
+        elif two_bot[nx]:
+            nx -= 1
+        ts.append(nx)
+    M = len(ts) - 1
+    last = np.empty(m, np.int64)  # last row of each column's block
+    for j, sz in blocks:
+        last[j:j + sz] = j + sz - 1
+    tile_of_row = np.repeat(np.arange(M), np.diff(ts))
+    tcol = tile_of_row[last]
+    per = []
+    for I in range(M - 1, 0, -1):
+        t0, t1 = ts[I], ts[I + 1]
+        full = np.count_nonzero(tcol > I) * (t1 - t0)
+        tip = last[tcol == I] - t0 + 1
+        per.append(4.0 * t0 * (full + tip.sum()))
+    return float(sum(per)), per, M
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_sample_select(blocks, m, nblk):
+    """every k-th eigenvalue block of the workload (stratified over r)"""
+    sel = np.zeros(m, np.int32)
+    idx = np.linspace(0, len(blocks) - 1, nblk).round().astype(int)
+    for b in np.unique(idx):
+        j, sz = blocks[b]
+        sel[j:j + sz] = 1
+    return sel
+
+
+def run_oracle_sample(S, T, blocks, m, nblk):
+    import oracle
+    sel = cpu_sample_select(blocks, m, nblk)
+    f = nominal_flops(blocks, sel)
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    r = oracle.tgevc(S, T, select=sel, nthreads=cores)
+    dt = time.perf_counter() - t
+    assert r["status"] == 0, r["status"]
+    return f, dt, cores, sel, r
+
+
+def workload_desc(name, cfg, mb):
+    return ("%s: m=%d FP64 Schur pencil, %d 2x2 blocks (%.0f%% of rows), off-diagonal N(0,%.3g), "
+            "per-eigenvalue separation >= %g, all eigenvectors, tile %d"
+            % (name, cfg["m"], cfg["n2"], 200.0 * cfg["n2"] / cfg["m"], cfg["var_off"],
+               cfg.get("gap", 0.0), mb))
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def reference_arm(args):
+    """--impl reference: the oracle as it stands on the host cores, bounded sample per step."""
+    cfg = dict(gen.CONFIGS[args.config])
+    m = cfg["m"]
+    S, T, _ = gen.config(args.config, seed=args.seed)
+    sub = np.diagonal(S, -1).copy()
+    blocks = blocks_from_sub(sub, m)
+    nblk = args.ref_blocks
+    for _ in range(args.warmup):
+        run_oracle_sample(S, T, blocks, m, nblk)
+    ts = []
+    f = 0.0
+    cores = os.cpu_count() or 1
+    for _ in range(args.steps):
+        f, dt, cores, sel, _ = run_oracle_sample(S, T, blocks, m, nblk)
+        ts.append(dt)
+    t = float(np.mean(ts))
+    val = f / t * 1e-12
+    sample = ("%d of %d eigenvalue blocks (every %d-th, stratified over r) of the %s pencil; "
+              "F_sample = %.4g flop per step" % (nblk, len(blocks), max(1, len(blocks) // nblk),
+                                                 args.config, f))
+    emit({"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+          "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+          "config": {"workload": workload_desc(args.config, cfg, args.mb), "m": m,
+                     "flops_per_step": f, "sample": sample},
+          "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+          "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--mb", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-blocks", type=int, default=192)
+    ap.add_argument("--ref-blocks", type=int, default=24)
+    ap.add_argument("--nb", type=int, default=64, help="column-block width of the multi-GPU shard")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args)
+        return
+
+    import torch
+    import paper_2003_04776_b200 as zz
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(gen.CONFIGS[args.config])
+    m = cfg["m"]
+    mb = args.mb
+    zz.init(local)
+    zz.set_tile(mb)
+    dev = torch.device("cuda", local)
+
+    # ---- inputs: generated on the host (pinned), resident in HBM before timing ----
+    Sh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True) if rank == 0 else None
+    Th = zz.empty_colmajor(m, m, device="cpu", pin_memory=True) if rank == 0 else None
+    if rank == 0:
+        gen.config(args.config, seed=args.seed, out=(Sh.data_ptr(), Th.data_ptr()))
+    Sd = zz.empty_colmajor(m, m, device=dev)
+    Td = zz.empty_colmajor(m, m, device=dev)
+    if rank == 0:
+        Sd.copy_(Sh)
+        Td.copy_(Th)
+        sub = torch.diagonal(Sh, -1).numpy().copy()
+    else:
+        sub = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [sub]
+        dist.broadcast_object_list(obj, src=0)
+        sub = obj[0]
+    blocks = blocks_from_sub(sub, m)
+    F = nominal_flops(blocks)
+    F_upd, per_launch, M = update_flops(blocks, m, mb)
+
+    Xd = zz.empty_colmajor(m, m, device=dev) if (rank == 0 or world == 1) else None
+    Ed = torch.empty(m, dtype=torch.int32, device=dev)
+
+    def step():
+        if world == 1:
+            zz.tgevc(Sd, Td, X=Xd, col_scale_exp=Ed)
+        else:
+            from paper_2003_04776_b200 import dist as zdist
+
+            def compute(S_, T_, sel):
+                return zz.tgevc(S_, T_, select=sel)
+            zdist.tgevc_distributed(Sd, Td, rank, world, compute, nb=args.nb, sub=sub)
+
+    zz.set_timing(True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    upd_ms = 0.0
+    launches = 0
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+        inf = zz.last_info()
+        upd_ms += inf["ms_update"]
+        launches += inf["total_launches"]
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.stop()
+    t = e0.elapsed_time(e1) / 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    value = F / t * 1e-12
+    zz.set_timing(False)
+    info = zz.last_info()
+
+    res = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_desc(args.config, cfg, mb), "m": m, "mb": mb, "tiles": M,
+                      "seconds_per_step": t, "flops_per_step": F,
+                      "fraction_of_fp64_peak": value / (FP64_PEAK * world),
+                      "l2": "inputs larger than L2 (S, T %.1f GB each; L2 126 MB)" % (m * m * 8 / 1e9),
+                      "parallelism": "replicated S,T; cyclic column blocks nb=%d" % args.nb if world > 1 else "1 GPU",
+                      "phase_ms_last_step": {k: info[k] for k in ("ms_setup", "ms_steps", "ms_normalize")}},
+           "gpu_launches": launches}
+    # roofline of the dominant kernel (the robust update, k_update)
+    upd_avg = upd_ms / max(1, args.steps * max(1, len(per_launch)))
+    if upd_ms > 0:
+        ach = (F_upd / len(per_launch)) / (upd_avg * 1e-3) * 1e-12
+        res["roofline"] = {"bound": "tensor", "kernel": "k_update (DMMA.8x8x4 FP64 contraction)",
+                           "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
+                           "traffic": None, "peak_source": PEAK_SRC,
+                           "algorithmic_flops_per_launch": F_upd / len(per_launch),
+                           "avg_launch_ms": upd_avg,
+                           "share_of_step": upd_ms / args.steps / (t * 1e3)}
+    res["clocks"] = clocks
+    if rank == 0 and world == 1 and not args.no_e2e:
+        # end to end through the public API with HOST buffers (pinned), copies inside
+        Xh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True)
+        Eh = torch.empty(m, dtype=torch.int32).pin_memory()
+        zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
+        ks = max(1, args.e2e_steps)
+        t0 = time.perf_counter()
+        for _ in range(ks):
+            zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
+        te = (time.perf_counter() - t0) / ks
+        res["e2e"] = {"value": F / te * 1e-12, "unit": "TFLOP/s", "seconds_per_step": te,
+                      "h2d_bytes_per_step": 2 * m * m * 8, "d2h_bytes_per_step": m * m * 8 + m * 4,
+                      "steps": ks, "api": "zz_tgevc_host (pinned host S, T, X)"}
+        Xd_check = Xd
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Sn, Tn = Sh.numpy(), Th.numpy()
+        f, dt, cores, sel, r = run_oracle_sample(Sn, Tn, blocks, m, args.cpu_blocks)
+        res["cpu_baseline"] = {"value": f / dt * 1e-12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                               "seconds": dt,
+                               "sample": "%d eigenvalue blocks (stratified over r) of the same pencil, "
+                                         "F_sample = %.4g flop, oracle/ as it stands, %d threads"
+                                         % (args.cpu_blocks, f, cores)}
+        # sampled full-size parity of the timed launch configuration vs the oracle
+        cols = np.flatnonzero(sel)
+        Xg = Xd[:, torch.as_tensor(cols, device=dev)].cpu().numpy()
+        Xo = r["X"]
+        err = []
+        for (j, sz) in blocks:
+            if not sel[j]:
+                continue
+            k = np.searchsorted(cols, j)
+            if sz == 1:
+                a, b = Xg[:, k], Xo[:, k]
+            else:
+                a = Xg[:, k] + 1j * Xg[:, k + 1]
+                b = Xo[:, k] + 1j * Xo[:, k + 1]
+            err.append(np.linalg.norm(a - b) / np.linalg.norm(b))
+        res["parity_sample"] = {"columns": int(len(cols)), "max_rel_2norm": float(max(err)),
+                                "median": float(np.median(err)), "tolerance": 1e-10}
+    if rank == 0:
+        emit(res)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,353 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI against the oracle on the
+same seeded inputs, plus invariants, edge cases, error codes, the scaling path and the
+full-size configurations in the launch configuration bench.py times.
+
+Tolerances: BASELINE.json north_star fixes the bar: every normalised column within 1e-10
+relative 2-norm of the oracle (phase-aligned for pairs; raw as well since both sides use
+the tip rule of reading R10) on the moderate-growth configs, and the normwise residual
+<= 10 m 2^-53 (reading R7).  Bitwise equality is required where the arithmetic is
+identical by construction (column independence / sharding, leading dimensions,
+power-of-two equivariance)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests import checks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def zz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2003_04776_b200 as zz
+    zz.init(0)
+    yield zz
+    zz.set_tile(0)
+
+
+def to_dev(A, ld=None):
+    m, n = A.shape
+    ld = ld or m
+    buf = torch.zeros((max(n, 1), ld), dtype=torch.float64, device="cuda")
+    buf[:n, :m] = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    return buf.t()[:m, :n]
+
+
+def solve(zz, S, T, mb=0, select=None, lds=None, ldx=None, Sd=None, Td=None):
+    zz.set_tile(mb)
+    m = S.shape[0] if S is not None else Sd.shape[0]
+    if Sd is None:
+        Sd, Td = to_dev(S, lds), to_dev(T, lds)
+    n = oracle.count_columns(S, select) if S is not None else m
+    X = None
+    if ldx is not None:
+        X = torch.full((max(n, 1), ldx), np.nan, dtype=torch.float64, device="cuda").t()[:m, :n]
+    X, e = zz.tgevc(Sd, Td, select=select, X=X, n_sel=n)
+    torch.cuda.synchronize()
+    return X.cpu().numpy(), e.cpu().numpy(), zz.last_info()
+
+
+def check_against_oracle(S, T, X, e, select=None, tol=TOL, ref=None):
+    ref = ref or oracle.tgevc(S, T, select=select)
+    assert ref["status"] == 0
+    lay = checks.column_layout(None, None, S, select)
+    raw, ali = checks.parity(X, ref["X"], lay)
+    assert np.isfinite(X).all()
+    assert ali.max() <= tol, (ali.max(), int(np.argmax(ali)))
+    assert raw.max() <= tol, (raw.max(), int(np.argmax(raw)))
+    # invariants: e <= 0, equal pair exponents, exact zeros below, LAPACK normalisation
+    assert (e <= 0).all()
+    for col, j, sz in lay:
+        assert np.all(X[j + sz:, col:col + sz] == 0.0)
+        if sz == 2:
+            assert e[col] == e[col + 1]
+            mx = np.max(np.abs(X[:, col]) + np.abs(X[:, col + 1]))
+        else:
+            mx = np.max(np.abs(X[:, col]))
+        assert abs(mx - 1.0) <= 4 * U
+    D, B, _ = checks.build_DB(ref["pairs"], S, select)
+    if S.shape[0] <= 3000:
+        res = checks.residual(S, T, X, D, B)
+        assert res <= 10 * S.shape[0] * U, res
+    return ref, raw, ali
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_C1_parity(zz, seed):
+    S, T, _ = gen.config("C1", seed=seed)
+    X, e, info = solve(zz, S, T, mb=32)
+    assert info["n_tiles"] >= 3
+    check_against_oracle(S, T, X, e)
+
+
+@pytest.mark.parametrize("mb", [32, 64, 96, 128, 160])
+def test_C2_parity_tile_sweep(zz, mb):
+    S, T, _ = gen.config("C2", seed=0)
+    X, e, info = solve(zz, S, T, mb=mb)
+    check_against_oracle(S, T, X, e)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 31, 33, 65, 130, 257, 511, 1025])
+def test_ragged_sizes(zz, m):
+    n2 = (3 * m) // 20
+    S, T, _ = gen.generate(m, n2, 1.0 / m, seed=m, gap_mode=2, gap=1e-4)
+    for mb in (32, 48, 160):
+        X, e, info = solve(zz, S, T, mb=mb)
+        check_against_oracle(S, T, X, e)
+
+
+def test_all_pairs_and_all_real(zz):
+    for m, n2 in [(64, 32), (66, 33), (100, 0)]:
+        S, T, _ = gen.generate(m, n2, 1.0 / m, seed=7, gap_mode=2, gap=1e-4)
+        X, e, _ = solve(zz, S, T, mb=32)
+        check_against_oracle(S, T, X, e)
+
+
+def test_zero_infinite_indefinite_negative(zz):
+    S, T, _ = gen.generate(300, 45, 1.0 / 300, seed=11, gap_mode=2, gap=1e-4, n_zero=4, n_inf=5)
+    # a negative T diagonal entry and an indefinite 1x1 block
+    d = [j for j in range(1, 299) if S[j, j - 1] == 0 and S[j + 1, j] == 0 and T[j, j] != 0]
+    T[d[3], d[3]] *= -1
+    S[d[7], d[7]] = 0.0
+    T[d[7], d[7]] = 0.0
+    X, e, info = solve(zz, S, T, mb=64)
+    assert info["n_indefinite"] == 1
+    check_against_oracle(S, T, X, e)
+    assert np.array_equal(X[:, d[7]], np.eye(300)[:, d[7]])
+
+
+def test_error_codes(zz):
+    # 2x2 block with real eigenvalues -> +j (1-based first row), as DTGEVC
+    S = np.array([[0.5, 0.1, 0.2, 0.1], [0.0, 1.0, 0.3, 0.2], [0.0, 1.0, 1.0, 0.3], [0, 0, 0, 2.0]], order="F")
+    T = np.eye(4, order="F")
+    with pytest.raises(zz.ZZError) as ei:
+        solve(zz, S, T, mb=32)
+    assert ei.value.status == 2 == oracle.tgevc(S, T)["status"]
+    # overlapping 2x2 blocks -> -105
+    S2 = S.copy()
+    S2[3, 2] = 1.0
+    with pytest.raises(zz.ZZError) as ei:
+        solve(zz, S2, T, mb=32)
+    assert ei.value.status == -105
+    # non-finite diagonal block -> -104
+    S3 = np.triu(S)
+    S3[1, 1] = np.inf
+    with pytest.raises(zz.ZZError) as ei:
+        solve(zz, S3, T, mb=32)
+    assert ei.value.status == -104
+
+
+def test_select_subsets_bitwise(zz):
+    S, T, _ = gen.config("C2", seed=1)
+    m = S.shape[0]
+    Xf, ef, _ = solve(zz, S, T, mb=64)
+    lay = checks.column_layout(None, None, S)
+    rng = np.random.default_rng(5)
+    for frac in (0.001, 0.05, 0.5):
+        sel = (rng.random(m) < frac).astype(np.int32)
+        Xs, es, _ = solve(zz, S, T, mb=64, select=sel)
+        cols = [c for (c, j, sz) in lay if sel[j] or (sz == 2 and sel[j + 1]) for c in range(c, c + sz)]
+        assert np.array_equal(Xs, Xf[:, cols])
+        assert np.array_equal(es, ef[cols])
+    # empty selection
+    Xs, es, info = solve(zz, S, T, mb=64, select=np.zeros(m, np.int32))
+    assert Xs.shape == (m, 0) and info["n_sel"] == 0
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_columns_bitwise(zz, P):
+    """the multi-GPU shard (cyclic column blocks, paper_2003_04776_b200/dist.py) computes each
+    rank's columns with select; assembled, X equals the 1-GPU X bitwise (per-column arithmetic
+    is independent of the other columns)."""
+    from paper_2003_04776_b200 import dist as zdist
+    S, T, _ = gen.config("C2", seed=2)
+    m = S.shape[0]
+    Xf, ef, _ = solve(zz, S, T, mb=128)
+    sub = np.diagonal(S, -1)
+    Xa = np.full_like(Xf, np.nan)
+    Ea = np.zeros_like(ef)
+    for r in range(P):
+        sel, cols = zdist.shard_select(sub, m, r, P, nb=64)
+        Xr, er, _ = solve(zz, S, T, mb=128, select=sel)
+        Xa[:, cols] = Xr
+        Ea[cols] = er
+    assert np.array_equal(Xa, Xf) and np.array_equal(Ea, ef)
+
+
+def test_leading_dimensions_and_alignment(zz):
+    S, T, _ = gen.config("C2", seed=0, m=700, n2=105)
+    X0, e0, _ = solve(zz, S, T, mb=64)
+    for lds, ldx in [(701, 703), (704, 700), (1001, 1001)]:
+        X1, e1, _ = solve(zz, S, T, mb=64, lds=lds, ldx=ldx)
+        assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
+
+
+def test_power_of_two_equivariance_and_prescale(zz):
+    S, T, _ = gen.config("C1", seed=6)
+    X0, e0, _ = solve(zz, S, T, mb=32)
+    for k in (-300, -5, 7, 200):
+        X1, e1, info = solve(zz, np.ldexp(S, k), np.ldexp(T, k), mb=32)
+        assert np.array_equal(X1, X0)
+    # entries near Omega/4: the pre-scale path (reading R6) must trigger and change nothing
+    X2, e2, info = solve(zz, np.ldexp(S, 1021), np.ldexp(T, 1021), mb=32)
+    assert info["prescaled"] == 1
+    assert np.array_equal(X2, X0)
+
+
+def _stress(m, seed, tile=32):
+    c = dict(gen.CONFIGS["C5"])
+    c.update(m=m, n2=(3 * m) // 20, stress_tile=tile)
+    return gen.generate(seed=seed, **c)[:2]
+
+
+@pytest.mark.parametrize("m,mb", [(1000, 64), (2000, 128)])
+def test_stress_scaling_path(zz, m, mb):
+    S, T = _stress(m, 0)
+    X, e, info = solve(zz, S, T, mb=mb)
+    ref = oracle.tgevc(S, T)
+    naive = oracle.tgevc(S, T, protect=False)
+    n_bad = int((~np.isfinite(naive["X"]).all(axis=0)).sum())
+    assert n_bad > 0                       # unprotected substitution overflows
+    assert np.isfinite(X).all()            # the robust GPU path does not
+    assert info["n_scaled"] > 0 and (e <= 0).all() and info["min_exp"] < 0
+    lay = checks.column_layout(None, None, S)
+    for col, j, sz in lay:
+        if sz == 2:
+            assert e[col] == e[col + 1]
+        assert np.all(X[j + sz:, col:col + sz] == 0.0)
+    w = checks.comp_backward_error(S, T, X, ref["pairs"], lay, m)
+    assert w <= 10 * m * U, w
+    D, B, _ = checks.build_DB(ref["pairs"], S)
+    assert checks.residual(S, T, X, D, B) <= 10 * m * U
+
+
+def _gpu_residual(Sd, Td, Xd, pairs, S_sub, cols=None):
+    """normwise residual (R7) on the GPU with FP64 GEMMs, for the column subset `cols`
+    (sorted; both columns of a pair present)"""
+    m = Sd.shape[0]
+    lay = checks.column_layout(None, None, S_sub)
+    D = np.zeros(m)
+    A = np.zeros(m)
+    Bc = np.zeros(m)
+    kind = np.zeros(m, int)          # 0 real, 1 first of pair, 2 second
+    for col, j, sz in lay:
+        a, b, be = pairs[j]
+        D[col:col + sz] = be
+        A[col:col + sz] = a
+        Bc[col:col + sz] = b
+        if sz == 2:
+            kind[col], kind[col + 1] = 1, 2
+    cols = np.arange(m) if cols is None else np.asarray(cols)
+    dev = "cuda"
+    Xc = Xd[:, torch.as_tensor(cols, device=dev)]
+    TX = Td @ Xc
+    R = (Sd @ Xc) * torch.as_tensor(D[cols], device=dev)
+    kc = kind[cols]
+    a_ = torch.as_tensor(A[cols], device=dev)
+    b_ = torch.as_tensor(Bc[cols], device=dev)
+    nxt = torch.as_tensor(np.minimum(np.arange(len(cols)) + 1, len(cols) - 1), device=dev)
+    prv = torch.as_tensor(np.maximum(np.arange(len(cols)) - 1, 0), device=dev)
+    first = torch.as_tensor(kc == 1, device=dev)
+    second = torch.as_tensor(kc == 2, device=dev)
+    XB = a_ * TX
+    XB = XB - torch.where(first, b_, torch.zeros_like(b_)) * TX[:, nxt]
+    XB = XB + torch.where(second, b_, torch.zeros_like(b_)) * TX[:, prv]
+    R = R - XB
+    num = torch.linalg.norm(R).item()
+    ab = np.hypot(A, Bc)
+    den = (torch.linalg.norm(Sd).item() * D.max() + torch.linalg.norm(Td).item() * ab.max()) * \
+        torch.linalg.norm(Xc).item()
+    return num / den
+
+
+@pytest.mark.slow
+def test_C3_full_parity(zz):
+    S, T, _ = gen.config("C3", seed=0)
+    Sd, Td = to_dev(S), to_dev(T)
+    zz.set_tile(128)
+    Xd, ed = zz.tgevc(Sd, Td)
+    torch.cuda.synchronize()
+    X, e = Xd.cpu().numpy(), ed.cpu().numpy()
+    ref = oracle.tgevc(S, T)
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(X, ref["X"], lay)
+    assert np.isfinite(X).all() and (e <= 0).all()
+    assert ali.max() <= TOL and raw.max() <= TOL, (raw.max(), ali.max())
+    assert _gpu_residual(Sd, Td, Xd, ref["pairs"], S) <= 10 * S.shape[0] * U
+
+
+@pytest.mark.slow
+def test_C5_stress_full(zz):
+    S, T, _ = gen.config("C5", seed=0)
+    m = S.shape[0]
+    Sd, Td = to_dev(S), to_dev(T)
+    zz.set_tile(128)
+    Xd, ed = zz.tgevc(Sd, Td)
+    torch.cuda.synchronize()
+    info = zz.last_info()
+    X, e = Xd.cpu().numpy(), ed.cpu().numpy()
+    assert np.isfinite(X).all() and (e <= 0).all()
+    lay = checks.column_layout(None, None, S)
+    for col, j, sz in lay:
+        if sz == 2:
+            assert e[col] == e[col + 1]
+    a, b, be, kd, st = oracle.eig_pairs(S, T)
+    pairs = np.stack([a, b, be], axis=1)
+    assert _gpu_residual(Sd, Td, Xd, pairs, S) <= 10 * m * U
+    # componentwise backward error on a sample of columns
+    rng = np.random.default_rng(0)
+    pick = sorted(rng.choice(len(lay), 60, replace=False))
+    sub_lay = [lay[i] for i in pick]
+    cols = [c for (c, j, sz) in sub_lay for c in range(c, c + sz)]
+    Xs = X[:, cols]
+    lay2, off = [], 0
+    for (c, j, sz) in sub_lay:
+        lay2.append((off, j, sz))
+        off += sz
+    assert checks.comp_backward_error(S, T, Xs, pairs, lay2, m) <= 10 * m * U
+
+
+@pytest.mark.slow
+def test_C4_full_size_sampled(zz):
+    """m = 40000 in the launch configuration bench.py times (mb = 128, all eigenvectors);
+    sampled columns against the oracle computed one by one."""
+    m = gen.CONFIGS["C4"]["m"]
+    Sd = torch.empty((m, m), dtype=torch.float64).pin_memory().t()
+    Td = torch.empty((m, m), dtype=torch.float64).pin_memory().t()
+    gen.config("C4", seed=0, out=(Sd.data_ptr(), Td.data_ptr()))
+    S, T = Sd.numpy(), Td.numpy()
+    Sg = torch.empty((m, m), dtype=torch.float64, device="cuda").t()
+    Tg = torch.empty((m, m), dtype=torch.float64, device="cuda").t()
+    Sg.copy_(Sd)
+    Tg.copy_(Td)
+    zz.set_tile(128)
+    Xd, ed = zz.tgevc(Sg, Tg)
+    torch.cuda.synchronize()
+    sub = np.diagonal(S, -1)
+    blocks = []
+    j = 0
+    while j < m:
+        sz = 2 if (j + 1 < m and sub[j] != 0) else 1
+        blocks.append((j, sz))
+        j += sz
+    rng = np.random.default_rng(1)
+    idx = sorted(set(rng.choice(len(blocks), 20, replace=False).tolist()) | {0, len(blocks) - 1})
+    sel = np.zeros(m, np.int32)
+    for b in idx:
+        jj, sz = blocks[b]
+        sel[jj:jj + sz] = 1
+    ref = oracle.tgevc(S, T, select=sel)
+    cols = np.flatnonzero(sel)
+    Xg = Xd[:, torch.as_tensor(cols, device="cuda")].cpu().numpy()
+    lay = checks.column_layout(None, None, S, sel)
+    raw, ali = checks.parity(Xg, ref["X"], lay)
+    assert np.isfinite(Xg).all()
+    assert ali.max() <= TOL and raw.max() <= TOL, (raw.max(), ali.max())
+    assert (ed.cpu().numpy() <= 0).all()
+    assert _gpu_residual(Sg, Tg, Xd, ref["pairs"], S, cols=cols) <= 10 * m * U
