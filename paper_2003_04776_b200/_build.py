@@ -14,7 +14,8 @@ def _stale():
     if not os.path.exists(SO):
         return True
     t = os.path.getmtime(SO)
-    deps = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))]
+    deps = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+            if f.endswith((".cu", ".cuh", ".h"))]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "zz.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
