@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -182,7 +183,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   for (int I = 0; I < M; ++I)
     for (int i = ts[I]; i < ts[I + 1]; ++i) row_tile[i] = I;
   // selection, packed columns, items (xTGEVC HOWMNY='S')
-  std::vector<int> blk_col((size_t)nb, -1), item_col, item_tile;
+  std::vector<int> blk_col((size_t)nb, -1), item_col, item_tile, item_two;
   std::vector<int> col_r, col_tile;
   int n_sel = 0;
   for (int p = 0; p < nb; ++p) {
@@ -192,6 +193,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     blk_col[p] = n_sel;
     item_col.push_back(n_sel);
     item_tile.push_back(row_tile[j]);
+    item_two.push_back(bz[p] == 2);
     for (int q = 0; q < bz[p]; ++q) {
       col_r.push_back(j + bz[p] - 1);
       col_tile.push_back(row_tile[j]);
@@ -207,13 +209,26 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     tile_item[I] = t;
     cs[I] = (t < n_items) ? item_col[t] : n_sel;
   }
+  // per-kind item lists (thread-per-eigenvector diagonal solve): ascending columns, and per
+  // tile row I the first entry whose eigenvalue block lies in a tile >= I
+  std::vector<int> real_list, pair_list, real_tile, pair_tile;
+  for (int t = 0; t < n_items; ++t) {
+    if (item_two[t]) { pair_list.push_back(item_col[t]); pair_tile.push_back(item_tile[t]); }
+    else { real_list.push_back(item_col[t]); real_tile.push_back(item_tile[t]); }
+  }
+  std::vector<int> rbeg((size_t)M + 1), pbeg((size_t)M + 1);
+  for (int I = 0; I <= M; ++I) {
+    rbeg[I] = (int)(std::lower_bound(real_tile.begin(), real_tile.end(), I) - real_tile.begin());
+    pbeg[I] = (int)(std::lower_bound(pair_tile.begin(), pair_tile.end(), I) - pair_tile.begin());
+  }
+  static const bool force_warp_diag = getenv("ZZ_DIAG_WARP") != nullptr;
   // ---- workspace ----
   const int n = std::max(n_sel, 1);
   const int nks_max = ceil_div(mb, kBK);
   const int n_ntiles_all = ceil_div(n, kBN);
   CK(c->colf.ensure(sizeof(double) * 3 * (size_t)n));
   CK(c->coli.ensure(sizeof(int) * 7 * (size_t)n));
-  CK(c->items.ensure(sizeof(int) * (size_t)std::max(n_items, 1)));
+  CK(c->items.ensure(sizeof(int) * 2 * (size_t)std::max(n_items, 1)));
   CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
   CK(c->rows.ensure((sizeof(int) + 1) * (size_t)m + 16));
   CK(c->blks.ensure(sizeof(int) * 3 * (size_t)nb));
@@ -233,6 +248,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.e_pend = P.col_tile + n;
   P.sY = P.e_pend + n;
   P.item_col = c->items.as<int>();
+  P.real_items = P.item_col + n_items;
+  P.pair_items = P.real_items + real_list.size();
   P.tile_start = c->tiles.as<int>();
   P.row_tile = c->rows.as<int>();
   P.row_flag = reinterpret_cast<signed char*>(P.row_tile + m);
@@ -259,6 +276,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     CK(cudaMemcpyAsync(P.col_r, col_r.data(), sizeof(int) * n_sel, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(P.col_tile, col_tile.data(), sizeof(int) * n_sel, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(P.item_col, item_col.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice, st));
+    if (!real_list.empty())
+      CK(cudaMemcpyAsync(P.real_items, real_list.data(), sizeof(int) * real_list.size(), cudaMemcpyHostToDevice, st));
+    if (!pair_list.empty())
+      CK(cudaMemcpyAsync(P.pair_items, pair_list.data(), sizeof(int) * pair_list.size(), cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemcpyAsync(P.tile_start, ts.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(P.row_tile, row_tile.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st));
@@ -374,7 +395,25 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     dp.X = X; dp.ldx = ldx;
     dp.P = P;
     dp.nY_in = I & 1;
-    CK(launch_diag(dp, st));
+    if (dp.nt <= kDiag2MaxNT && !force_warp_diag) {
+      Diag2Params d2;
+      d2.I = I; d2.t0 = dp.t0; d2.nt = dp.nt;
+      d2.n_real = (int)real_list.size() - rbeg[I];
+      d2.n_pair = (int)pair_list.size() - pbeg[I];
+      d2.real_items = P.real_items + rbeg[I];
+      d2.pair_items = P.pair_items + pbeg[I];
+      d2.tip_col_end = dp.tip_col_end;
+      d2.do_update = dp.do_update;
+      d2.nks = dp.nks;
+      d2.n_sel = n_sel;
+      d2.S = Su; d2.lds = ldsu; d2.T = Tu; d2.ldt = ldtu;
+      d2.X = X; d2.ldx = ldx;
+      d2.P = P;
+      d2.nY_in = dp.nY_in;
+      CK(launch_diag2(d2, st));
+    } else {
+      CK(launch_diag(dp, st));
+    }
     launches++;
     if (I > 0) {
       UpdParams up;

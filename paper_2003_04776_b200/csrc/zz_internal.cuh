@@ -61,6 +61,8 @@ struct DevPlan {
   int* col_tile;      // tile index of that block
   // per item (selected block) t
   int* item_col;      // first output column
+  int* real_items;    // columns of the selected real eigenvalues (ascending)
+  int* pair_items;    // first columns of the selected complex pairs (ascending)
   // per tile
   int* tile_start;    // M+1
   // per row
@@ -115,7 +117,28 @@ struct UpdParams {
   int vec;           // 16-byte aligned X access possible
 };
 
-// launchers (zz_kernels.cu / zz_update.cu)
+// Thread-per-eigenvector diagonal solve (zz_diag.cu): tiles of at most kDiag2MaxNT rows.
+constexpr int kDiag2MaxNT = 128;
+
+struct Diag2Params {
+  int I, t0, nt;
+  int n_real, n_pair;      // active real columns / complex pairs at this step
+  const int* real_items;   // their columns (ascending), already offset to the active suffix
+  const int* pair_items;   // first columns of the active pairs
+  int tip_col_end;         // columns < tip_col_end have their eigenvalue block in tile I
+  int do_update;
+  int nks;
+  int n_sel;
+  const double* S; long long lds;
+  const double* T; long long ldt;
+  double* X; long long ldx;
+  DevPlan P;
+  int nY_in;
+};
+
+// launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)
+cudaError_t launch_diag2(const Diag2Params& p, cudaStream_t st);
+size_t diag2_smem_bytes(int nt);
 cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, cudaStream_t st);
 cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int nblk,
                          const DevPlan& P, cudaStream_t st);

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "zz_internal.cuh"
+#include "zz_device.cuh"
 
 namespace zz {
 
@@ -30,9 +31,6 @@ cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, c
 // operation is an explicit round-to-nearest intrinsic (no contraction), so the pairs --
 // and hence the pivots beta S_ii - alpha T_ii -- are fixed bit patterns (reading R17).
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ double dmaxd(double x, double y) { return x > y ? x : y; }
-__device__ __forceinline__ double dmind(double x, double y) { return x < y ? x : y; }
-
 __device__ void normalise_pair(double& a, double& b, double& beta, int& kind) {
   double h = dmaxd(__dmul_rn(0.5, beta), __dadd_rn(__dmul_rn(0.5, fabs(a)), __dmul_rn(0.5, fabs(b))));
   if (h == 0.0) { kind = kIndefinite; return; }
@@ -288,28 +286,6 @@ __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
   return v;
-}
-
-struct cpx { double re, im; };
-__device__ __forceinline__ cpx mkc(double r, double i) { cpx z; z.re = r; z.im = i; return z; }
-__device__ __forceinline__ double n1(cpx z) { return __dadd_rn(fabs(z.re), fabs(z.im)); }
-__device__ __forceinline__ double nmax(cpx z) { return dmaxd(fabs(z.re), fabs(z.im)); }
-__device__ __forceinline__ cpx cmulx(cpx x, cpx y) {
-  return mkc(__dsub_rn(__dmul_rn(x.re, y.re), __dmul_rn(x.im, y.im)),
-             __dadd_rn(__dmul_rn(x.re, y.im), __dmul_rn(x.im, y.re)));
-}
-__device__ __forceinline__ cpx csubx(cpx x, cpx y) { return mkc(__dsub_rn(x.re, y.re), __dsub_rn(x.im, y.im)); }
-// Smith's division (reading R9)
-__device__ __forceinline__ cpx cdivx(cpx x, cpx y) {
-  if (fabs(y.re) >= fabs(y.im)) {
-    double r = __ddiv_rn(y.im, y.re), den = __dadd_rn(y.re, __dmul_rn(y.im, r));
-    return mkc(__ddiv_rn(__dadd_rn(x.re, __dmul_rn(x.im, r)), den),
-               __ddiv_rn(__dsub_rn(x.im, __dmul_rn(x.re, r)), den));
-  } else {
-    double r = __ddiv_rn(y.re, y.im), den = __dadd_rn(y.im, __dmul_rn(y.re, r));
-    return mkc(__ddiv_rn(__dadd_rn(__dmul_rn(x.re, r), x.im), den),
-               __ddiv_rn(__dsub_rn(__dmul_rn(x.im, r), x.re), den));
-  }
 }
 
 // shared context of one warp's eigenvector

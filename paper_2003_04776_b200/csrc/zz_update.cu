@@ -74,8 +74,33 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kCWarps * 32) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
-    k_update(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p) {
+// predicated global accesses (no branch around a load: every C load of a lane is issued
+// before the first one is consumed)
+__device__ __forceinline__ void ld2p(double& x, double& y, const double* p, bool pr) {
+  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q ld.global.v2.f64 {%0, %1}, [%2];\n}"
+      : "+d"(x), "+d"(y) : "l"(p), "r"((int)pr));
+}
+__device__ __forceinline__ void ld1p(double& x, const double* p, bool pr) {
+  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.global.f64 %0, [%1];\n}" : "+d"(x) : "l"(p), "r"((int)pr));
+}
+__device__ __forceinline__ void st2p(double* p, double x, double y, bool pr) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.global.v2.f64 [%0], {%1, %2};\n}"
+               ::"l"(p), "d"(x), "d"(y), "r"((int)pr) : "memory");
+}
+__device__ __forceinline__ void st1p(double* p, double x, bool pr) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.f64 [%0], %1;\n}"
+               ::"l"(p), "d"(x), "r"((int)pr) : "memory");
+}
+
+__device__ __forceinline__ void ld1p_i(int& x, const int* p, bool pr) {
+  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.global.b32 %0, [%1];\n}" : "+r"(x) : "l"(p), "r"((int)pr));
+}
+
+// Persistent: each CTA walks the (m-tile, n-tile) grid with stride gridDim.x; the producer
+// warp runs ahead into the next tile while the consumers finish the current epilogue.
+__global__ void __maxnreg__(200)
+    k_update(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
+             int n_mtiles, int n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
@@ -84,8 +109,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntile = p.ntile0 + blockIdx.x;
-  const int n0 = ntile * kBN, m0 = blockIdx.y * kBM;
   const int nkc = 2 * p.nks;
 
   if (threadIdx.x == 0) {
@@ -101,17 +124,22 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kCWarps) {
     // ---------------- producer: TMA (S/T chunks) + bulk copy (W chunk) ----------------
     if (lane == 0) {
-      const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
-      for (int kc = 0; kc < nkc; ++kc) {
-        const int s = kc % kStages;
-        if (kc >= kStages) mbar_wait(&empty[s], ((kc / kStages) - 1) & 1);
-        mbar_expect_tx(&full[s], kStageBytes);
-        const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
-        const int kcol = p.t0 + (kc % p.nks) * kBK;
-        double* a = sA + s * (kBM * kBK);
+      int g = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int m0 = (tile % n_mtiles) * kBM;
+        const int ntile = p.ntile0 + tile / n_mtiles;
+        const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
+        for (int kc = 0; kc < nkc; ++kc, ++g) {
+          const int s = g % kStages;
+          if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
+          mbar_expect_tx(&full[s], kStageBytes);
+          const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
+          const int kcol = p.t0 + (kc % p.nks) * kBK;
+          double* a = sA + s * (kBM * kBK);
 #pragma unroll 4
-        for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
-        bulk_load(sB + s * (kBN * kBK), wt + (long long)kc * (kBN * kBK), kBBytes, &full[s]);
+          for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
+          bulk_load(sB + s * (kBN * kBK), wt + (long long)kc * (kBN * kBK), kBBytes, &full[s]);
+        }
       }
     }
     return;
@@ -120,89 +148,98 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ---------------- consumers: 4 warps, 2 (rows) x 2 (columns), 64 x 32 each ----------------
   const int wm = warp >> 1, wn = warp & 1;
   const int rq = lane & 3, cq = lane >> 2;
-  double acc[4][8][2];
-  // accumulators start from the scaled pending values: 2^sY[c] * Y (exact)
+  int g = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int m0 = (tile % n_mtiles) * kBM;
+    const int n0 = (p.ntile0 + tile / n_mtiles) * kBN;
+    double acc[4][8][2];
+    // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
+    int sy[4];
 #pragma unroll
-  for (int ni = 0; ni < 4; ++ni) {
-    const int c = n0 + wn * 32 + ni * 8 + cq;
-    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
-    const bool ld = cvalid && (c >= p.first_end);
-    const int sy = ld ? p.sY[c] : 0;
-    const double* xc = p.X + (long long)c * p.ldx;
+    for (int ni = 0; ni < 4; ++ni) {
+      const int c = n0 + wn * 32 + ni * 8 + cq;
+      const bool ld = (c >= p.c_begin) && (c < p.n_sel) && (c >= p.first_end);
+      sy[ni] = 0;
+      ld1p_i(sy[ni], p.sY + (ld ? c : 0), ld);
+      const double* xc = p.X + (long long)(ld ? c : 0) * p.ldx;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
-      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
-      double v0 = 0.0, v1 = 0.0;
-      if (ld && i0 < p.rows) {
-        if (p.vec && i0 + 1 < p.rows) {
-          double2 t = *reinterpret_cast<const double2*>(xc + i0);
-          v0 = t.x; v1 = t.y;
-        } else {
-          v0 = xc[i0];
-          if (i0 + 1 < p.rows) v1 = xc[i0 + 1];
-        }
-        if (sy != 0) { v0 = ldexp(v0, sy); v1 = ldexp(v1, sy); }
+      for (int mi = 0; mi < 8; ++mi) {
+        const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+        const bool both = ld && (i0 + 1 < p.rows);
+        acc[ni][mi][0] = 0.0;
+        acc[ni][mi][1] = 0.0;
+        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, both && p.vec);
+        ld1p(acc[ni][mi][0], xc + i0, ld && i0 < p.rows && !(both && p.vec));
+        ld1p(acc[ni][mi][1], xc + i0 + 1, both && !p.vec);
       }
-      acc[ni][mi][0] = v0;
-      acc[ni][mi][1] = v1;
     }
-  }
-
-  for (int kc = 0; kc < nkc; ++kc) {
-    const int s = kc % kStages;
-    mbar_wait(&full[s], (kc / kStages) & 1);
-    const double* a = sA + s * (kBM * kBK);
-    const double* b = sB + s * (kBN * kBK);
 #pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      double fw[4], fs[8];
+    for (int ni = 0; ni < 4; ++ni) {
+      if (sy[ni] != 0) {
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wn * 32 + ni * 8 + cq) * 4 + rq];
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-
-  // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
-#pragma unroll
-  for (int ni = 0; ni < 4; ++ni) {
-    const int c = n0 + wn * 32 + ni * 8 + cq;
-    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
-    double* xc = p.X + (long long)c * p.ldx;
-    double cm = 0.0;
-#pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
-      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
-      const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
-      if (cvalid && i0 < p.rows) {
-        if (p.vec && i0 + 1 < p.rows) {
-          *reinterpret_cast<double2*>(xc + i0) = make_double2(v0, v1);
-        } else {
-          xc[i0] = v0;
-          if (i0 + 1 < p.rows) xc[i0 + 1] = v1;
+        for (int mi = 0; mi < 8; ++mi) {
+          acc[ni][mi][0] = ldexp(acc[ni][mi][0], sy[ni]);
+          acc[ni][mi][1] = ldexp(acc[ni][mi][1], sy[ni]);
         }
       }
-      if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
-      if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
     }
-    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-    if (rq == 0 && cvalid && cm > 0.0)
-      atomicMax(&colmax[c - n0], (unsigned long long)__double_as_longlong(cm));
-  }
-  consumer_sync();
-  if (threadIdx.x < kBN) {
-    const int c = n0 + threadIdx.x;
-    const unsigned long long v = colmax[threadIdx.x];
-    if (v != 0ull && c >= p.c_begin && c < p.n_sel) atomicMax(&p.nY_out[c], v);
+
+    for (int kc = 0; kc < nkc; ++kc, ++g) {
+      const int s = g % kStages;
+      mbar_wait(&full[s], (g / kStages) & 1);
+      const double* a = sA + s * (kBM * kBK);
+      const double* b = sB + s * (kBN * kBK);
+#pragma unroll
+      for (int ks = 0; ks < kBK / 4; ++ks) {
+        double fw[4], fs[8];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wn * 32 + ni * 8 + cq) * 4 + rq];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int c = n0 + wn * 32 + ni * 8 + cq;
+      const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
+      double* xc = p.X + (long long)(cvalid ? c : 0) * p.ldx;
+      double cm = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+        const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
+        const bool both = cvalid && (i0 + 1 < p.rows);
+        st2p(xc + i0, v0, v1, both && p.vec);
+        st1p(xc + i0, v0, cvalid && i0 < p.rows && !(both && p.vec));
+        st1p(xc + i0 + 1, v1, both && !p.vec);
+        if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
+        if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
+      }
+      cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+      cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+      if (rq == 0 && cvalid && cm > 0.0)
+        atomicMax(&colmax[c - n0], (unsigned long long)__double_as_longlong(cm));
+    }
+    consumer_sync();
+    if (threadIdx.x < kBN) {
+      const int c = n0 + threadIdx.x;
+      const unsigned long long v = colmax[threadIdx.x];
+      if (v != 0ull && c >= p.c_begin && c < p.n_sel) atomicMax(&p.nY_out[c], v);
+      colmax[threadIdx.x] = 0ull;
+    }
+    consumer_sync();
   }
 }
+
+static int g_upd_sms = 0;
 
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st) {
@@ -210,11 +247,15 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_upd_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
-  dim3 grid(n_ntiles, n_mtiles);
-  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
+  const int n_tiles = n_mtiles * n_ntiles;
+  const int grid = n_tiles < 2 * g_upd_sms ? n_tiles : 2 * g_upd_sms;
+  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
   return cudaGetLastError();
 }
 
