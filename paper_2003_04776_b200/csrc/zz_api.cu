@@ -221,7 +221,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     rbeg[I] = (int)(std::lower_bound(real_tile.begin(), real_tile.end(), I) - real_tile.begin());
     pbeg[I] = (int)(std::lower_bound(pair_tile.begin(), pair_tile.end(), I) - pair_tile.begin());
   }
-  static const bool force_warp_diag = getenv("ZZ_DIAG_WARP") != nullptr;
+  // diagonal-solve kernel: 3 = 8 columns per warp with DMMA in-tile updates (default),
+  // 2 = thread per eigenvector with sub-tile warps, 1 = warp per eigenvector (any tile)
+  static const int diag_kind = getenv("ZZ_DIAG") ? atoi(getenv("ZZ_DIAG")) : 3;
   // ---- workspace ----
   const int n = std::max(n_sel, 1);
   const int nks_max = ceil_div(mb, kBK);
@@ -395,7 +397,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     dp.X = X; dp.ldx = ldx;
     dp.P = P;
     dp.nY_in = I & 1;
-    if (dp.nt <= kDiag2MaxNT && !force_warp_diag) {
+    if (dp.nt <= kDiag2MaxNT && diag_kind >= 2) {
       Diag2Params d2;
       d2.I = I; d2.t0 = dp.t0; d2.nt = dp.nt;
       d2.n_real = (int)real_list.size() - rbeg[I];
@@ -410,7 +412,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.X = X; d2.ldx = ldx;
       d2.P = P;
       d2.nY_in = dp.nY_in;
-      CK(launch_diag2(d2, st));
+      CK(diag_kind == 2 ? launch_diag2(d2, st) : launch_diag3(d2, st));
     } else {
       CK(launch_diag(dp, st));
     }

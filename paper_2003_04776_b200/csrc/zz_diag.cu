@@ -45,6 +45,15 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// x * 2^k for k <= 0 (exact while the result is normal; powers of two below 2^-1022 are
+// applied in steps).  Much shorter code than ldexp in the unrolled register loops.
+__device__ __forceinline__ double pow2i(int k) { return __hiloint2double((k + 1023) << 20, 0); }
+__device__ __noinline__ double scale2_slow(double x, int k) {
+  while (k < -1022) { x *= 0x1p-1022; k += 1022; }
+  return x * pow2i(k);
+}
+__device__ __forceinline__ double scale2(double x, int k) { return k >= -1022 ? x * pow2i(k) : scale2_slow(x, k); }
+
 struct Sm {
   double2* ST;       // packed upper tile (+ subdiagonal): (S_ij, T_ij) at poff2(j) + i
   double2* cm;       // per row j: max |S|, |T| over the sub-tile rows above j's block
@@ -115,7 +124,7 @@ __device__ __forceinline__ cpx pdiv_v(cpx z, cpx d, int& k) {
 
 // 1x1 row: (beta S_jj - alpha T_jj) x = w
 template <bool PAIR>
-__device__ __noinline__ cpx micro1(cpx w, double sjj, double tjj, double a, double b, double beta, double ab,
+__device__ __forceinline__ cpx micro1(cpx w, double sjj, double tjj, double a, double b, double beta, double ab,
                                    int& k) {
   cpx d = mkc(__fma_rn(-a, tjj, __dmul_rn(beta, sjj)), __dmul_rn(-b, tjj));
   double smin = dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, fabs(sjj)), __dmul_rn(ab, fabs(tjj)))), kSmlnum);
@@ -126,7 +135,7 @@ __device__ __noinline__ cpx micro1(cpx w, double sjj, double tjj, double a, doub
 
 // 2x2 rows (top, bot): complete pivoting on |Re|+|Im|, pivots below smin -> smin.
 template <bool PAIR>
-__device__ __noinline__ void micro2(cpx& wt, cpx& wb, double s11, double s21, double s12, double s22, double t11,
+__device__ __forceinline__ void micro2(cpx& wt, cpx& wb, double s11, double s21, double s12, double s22, double t11,
                                     double t12, double t22, double a, double b, double beta, double ab, int& k) {
   cpx C[2][2];
   C[0][0] = mkc(__fma_rn(-a, t11, __dmul_rn(beta, s11)), __dmul_rn(-b, t11));
@@ -181,10 +190,29 @@ __device__ __noinline__ void micro2(cpx& wt, cpx& wb, double s11, double s21, do
 
 template <bool PAIR>
 __device__ __forceinline__ void scale_regs(double (&yr)[kSR], double (&yi)[kSR], int k) {
+  while (k < -1022) {
+#pragma unroll
+    for (int i = 0; i < kSR; ++i) {
+      yr[i] *= 0x1p-1022;
+      if (PAIR) yi[i] *= 0x1p-1022;
+    }
+    k += 1022;
+  }
+  const double f = pow2i(k);
 #pragma unroll
   for (int i = 0; i < kSR; ++i) {
-    yr[i] = ldexp(yr[i], k);
-    if (PAIR) yi[i] = ldexp(yi[i], k);
+    yr[i] *= f;
+    if (PAIR) yi[i] *= f;
+  }
+}
+
+// the same on the lane's column of a published sub-tile in shared memory (rows < n)
+__device__ __forceinline__ void scale_smem(double2* x, int n, int k) {
+  for (int i = 0; i < n; ++i) {
+    double2 v = x[i * kXP];
+    v.x = scale2(v.x, k);
+    v.y = scale2(v.y, k);
+    x[i * kXP] = v;
   }
 }
 
@@ -197,23 +225,6 @@ __device__ __forceinline__ double max_rows(const double (&yr)[kSR], const double
   return m;
 }
 
-
-// rows i < n of the sub-tile <- y_i - S_i,src (beta x) + T_i,src (alpha x)
-template <bool PAIR>
-__device__ __forceinline__ void upd_rows(double (&yr)[kSR], double (&yi)[kSR], const double2* col, double xr,
-                                         double xi, int n, double a, double b, double beta) {
-  const double ur = beta * xr, ui = beta * xi;
-  const double wr = PAIR ? (a * xr - b * xi) : a * xr;
-  const double wi = PAIR ? (a * xi + b * xr) : 0.0;
-#pragma unroll
-  for (int i = 0; i < kSR; ++i) {
-    if (i < n) {
-      const double2 st = col[i];
-      yr[i] = fma(st.y, wr, fma(-st.x, ur, yr[i]));
-      if (PAIR) yi[i] = fma(st.y, wi, fma(-st.x, ui, yi[i]));
-    }
-  }
-}
 
 // ------------------------------------------------------------------------------------
 // One group of (up to) 32 eigenvectors of one kind.
@@ -261,8 +272,8 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
       const int ek = sm.xe[k2 * 32 + lane];
       const double ymax = max_rows<PAIR>(yr, yi, len);
       const int g = min(ex, ek);
-      const double yh = (g != ex) ? ldexp(ymax, g - ex) : ymax;
-      const double xh = (g != ek) ? ldexp(xnv, g - ek) : xnv;
+      const double yh = (g != ex) ? scale2(ymax, g - ex) : ymax;
+      const double xh = (g != ek) ? scale2(xnv, g - ek) : xnv;
       const double2 nbv = sm.nb[warp * kNSub + k2];
       const double tau = __dadd_rn(__dmul_rn(beta, nbv.x), __dmul_rn(ab, nbv.y));
       const int en = g + protect_update(yh, tau, xh);
@@ -273,7 +284,7 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
       for (int l = len2 - 1; l >= 0; --l) {
         const double2 xv = xsk[l * kXP];
         double xr = xv.x, xi = xv.y;
-        if (sx != 0) { xr = ldexp(xr, sx); xi = ldexp(xi, sx); }
+        if (sx != 0) { xr = scale2(xr, sx); xi = scale2(xi, sx); }
         // u = x D (beta x), w = x B (alpha x)
         const double ur = beta * xr, ui = beta * xi;
         const double wr = PAIR ? (a * xr - b * xi) : a * xr;
@@ -290,72 +301,103 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
       }
     }
     // ---- bottom-up substitution inside the sub-tile ----
+    // The lane's column of the sub-tile moves to its slot of the exchange buffer, where the
+    // row loop can index it at run time (short code; the structure is per row, so the
+    // control flow stays uniform across the warp).
+    double2* xw = sm.xs + (warp * kSR) * kXP + lane;
 #pragma unroll
-    for (int j = kSR - 1; j >= 0; --j) {
-      if (j < len) {
-        const int gj = r0 + j;
-        const signed char f = sm.fl[gj];
-        if (f != kRowTop2) {
-          int js = j;
-          int k = 0;
-          if (j > 0 && f == kRowBot2) {
-            const int jt = (j > 0) ? j - 1 : 0;
-            js = j - 1;
-            const double2 d11 = sm.ST[poff2(gj - 1) + gj - 1], d21 = sm.ST[poff2(gj - 1) + gj];
-            const double2 d12 = sm.ST[poff2(gj) + gj - 1], d22 = sm.ST[poff2(gj) + gj];
-            cpx wt = mkc(yr[jt], PAIR ? yi[jt] : 0.0), wb = mkc(yr[j], PAIR ? yi[j] : 0.0);
-            micro2<PAIR>(wt, wb, d11.x, d21.x, d12.x, d22.x, d11.y, d12.y, d22.y, a, b, beta, ab, k);
-            if (PAIR && tip && tipr == gj) {
-              // tip of a complex pair (reading R10): rows (r-1, r) of the eigenvalue block
-              const double pp = __dmul_rn(beta, d21.x);
-              const cpx q = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
-              if (fabs(pp) >= n1(q)) {
-                wb = mkc(1.0, 0.0);
-                wt = mkc(__ddiv_rn(-q.re, pp), __ddiv_rn(-q.im, pp));
-              } else {
-                wt = mkc(1.0, 0.0);
-                const cpx z = cdivx(mkc(pp, 0.0), q);
-                wb = mkc(-z.re, -z.im);
-              }
-              k = 0;
-            }
-            if (k < 0) { scale_regs<PAIR>(yr, yi, k); ex += k; }
-            yr[jt] = wt.re; yr[j] = wb.re;
-            if (PAIR) { yi[jt] = wt.im; yi[j] = wb.im; }
+    for (int i = 0; i < kSR; ++i)
+      if (i < len) xw[i * kXP] = make_double2(yr[i], PAIR ? yi[i] : 0.0);
+    int j = len - 1;
+    while (j >= 0) {
+      const int gj = r0 + j;
+      const bool two = sm.fl[gj] == kRowBot2;
+      const int js = two ? j - 1 : j;
+      int k = 0;
+      cpx xt, xb;   // solution of rows js (top) and j (bottom)
+      if (two) {
+        const double2 d11 = sm.ST[poff2(gj - 1) + gj - 1], d21 = sm.ST[poff2(gj - 1) + gj];
+        const double2 d12 = sm.ST[poff2(gj) + gj - 1], d22 = sm.ST[poff2(gj) + gj];
+        const double2 vt = xw[(j - 1) * kXP], vb = xw[j * kXP];
+        xt = mkc(vt.x, vt.y);
+        xb = mkc(vb.x, vb.y);
+        micro2<PAIR>(xt, xb, d11.x, d21.x, d12.x, d22.x, d11.y, d12.y, d22.y, a, b, beta, ab, k);
+        if (PAIR && tip && tipr == gj) {
+          // tip of a complex pair (reading R10): rows (r-1, r) of the eigenvalue block
+          const double pp = __dmul_rn(beta, d21.x);
+          const cpx q = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
+          if (fabs(pp) >= n1(q)) {
+            xb = mkc(1.0, 0.0);
+            xt = mkc(__ddiv_rn(-q.re, pp), __ddiv_rn(-q.im, pp));
           } else {
-            const double2 d = sm.ST[poff2(gj) + gj];
-            cpx x = micro1<PAIR>(mkc(yr[j], PAIR ? yi[j] : 0.0), d.x, d.y, a, b, beta, ab, k);
-            if (!PAIR && tip && tipr == gj) { x = mkc(1.0, 0.0); k = 0; }
-            if (k < 0) { scale_regs<PAIR>(yr, yi, k); ex += k; }
-            yr[j] = x.re;
-            if (PAIR) yi[j] = x.im;
+            xt = mkc(1.0, 0.0);
+            const cpx z = cdivx(mkc(pp, 0.0), q);
+            xb = mkc(-z.re, -z.im);
           }
-          // in-sub-tile update of the rows above the block (ProtectUpdate)
-          if (js > 0) {
-            double t = 0.0;
-            for (int kk = js; kk <= j; ++kk) {
-              const double2 cmv = sm.cm[r0 + kk];
-              t = __dadd_rn(t, __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y)));
-            }
-            const int jt = (j > 0) ? j - 1 : 0;
-            double xnb = PAIR ? fmax(fabs(yr[j]), fabs(yi[j])) : fabs(yr[j]);
-            if (js < j) xnb = dmaxd(PAIR ? fmax(fabs(yr[jt]), fabs(yi[jt])) : fabs(yr[jt]), xnb);
-            const double ym = max_rows<PAIR>(yr, yi, js);
-            const int eu = protect_update(ym, t, xnb);
-            if (eu < 0) { scale_regs<PAIR>(yr, yi, eu); ex += eu; }
-            // sources in ascending row order, as the oracle's O6
-            if (js < j) upd_rows<PAIR>(yr, yi, sm.ST + poff2(r0 + jt) + r0, yr[jt], PAIR ? yi[jt] : 0.0, js, a, b, beta);
-            upd_rows<PAIR>(yr, yi, sm.ST + poff2(r0 + j) + r0, yr[j], PAIR ? yi[j] : 0.0, js, a, b, beta);
+          k = 0;
+        }
+      } else {
+        const double2 d = sm.ST[poff2(gj) + gj];
+        const double2 v = xw[j * kXP];
+        xb = micro1<PAIR>(mkc(v.x, v.y), d.x, d.y, a, b, beta, ab, k);
+        if (!PAIR && tip && tipr == gj) { xb = mkc(1.0, 0.0); k = 0; }
+        xt = xb;
+      }
+      if (k < 0) { scale_smem(xw, len, k); ex += k; }
+      // in-sub-tile update of the rows above the block (ProtectUpdate)
+      if (js > 0) {
+        double t = 0.0;
+        for (int kk = js; kk <= j; ++kk) {
+          const double2 cmv = sm.cm[r0 + kk];
+          t = __dadd_rn(t, __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y)));
+        }
+        double xnb = PAIR ? nmax(xb) : fabs(xb.re);
+        if (two) xnb = dmaxd(PAIR ? nmax(xt) : fabs(xt.re), xnb);
+        double ym = 0.0;
+        for (int i = 0; i < js; ++i) {
+          const double2 v = xw[i * kXP];
+          ym = fmax(ym, PAIR ? fmax(fabs(v.x), fabs(v.y)) : fabs(v.x));
+        }
+        const int eu = protect_update(ym, t, xnb);
+        if (eu < 0) {
+          scale_smem(xw, len, eu);   // the whole sub-tile: solved rows too
+          ex += eu;
+          xt = mkc(scale2(xt.re, eu), scale2(xt.im, eu));
+          xb = mkc(scale2(xb.re, eu), scale2(xb.im, eu));
+        }
+        // sources in ascending row order, as the oracle's O6
+        for (int s2 = two ? 0 : 1; s2 < 2; ++s2) {
+          const cpx x = s2 ? xb : xt;
+          const double ur = beta * x.re, ui = beta * x.im;
+          const double wr = PAIR ? (a * x.re - b * x.im) : a * x.re;
+          const double wi = PAIR ? (a * x.im + b * x.re) : 0.0;
+          const double2* col = sm.ST + poff2(r0 + (s2 ? j : js)) + r0;
+#pragma unroll 4
+          for (int i = 0; i < js; ++i) {
+            const double2 st = col[i];
+            double2 v = xw[i * kXP];
+            v.x = fma(st.y, wr, fma(-st.x, ur, v.x));
+            if (PAIR) v.y = fma(st.y, wi, fma(-st.x, ui, v.y));
+            xw[i * kXP] = v;
           }
         }
       }
+      if (two) xw[(j - 1) * kXP] = make_double2(xt.re, PAIR ? xt.im : 0.0);
+      xw[j * kXP] = make_double2(xb.re, PAIR ? xb.im : 0.0);
+      j = js - 1;
     }
-    // ---- publish the solved sub-tile ----
-    double2* xo = sm.xs + (warp * kSR) * kXP + lane;
+    // ---- publish the solved sub-tile (already in place in the exchange buffer) ----
+    double xm = 0.0;
 #pragma unroll
-    for (int i = 0; i < kSR; ++i)
-      if (i < len) xo[i * kXP] = make_double2(yr[i], PAIR ? yi[i] : 0.0);
-    sm.xn[warp * 32 + lane] = max_rows<PAIR>(yr, yi, len);
+    for (int i = 0; i < kSR; ++i) {
+      if (i < len) {
+        const double2 v = xw[i * kXP];
+        yr[i] = v.x;
+        yi[i] = v.y;
+        xm = fmax(xm, PAIR ? fmax(fabs(v.x), fabs(v.y)) : fabs(v.x));
+      }
+    }
+    sm.xn[warp * 32 + lane] = xm;
     sm.xe[warp * 32 + lane] = ex;
     if (warp > 0) {
       __threadfence_block();
@@ -414,7 +456,7 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
       // Alg. 3 with Alg. 2, reading R5
       const double nyv = tip ? 0.0 : __longlong_as_double((long long)P.nY[(long long)p.nY_in * p.n_sel + c]);
       const int g = min(ep, es);
-      const double yh = ldexp(nyv, g - ep), xh = ldexp(nrm, g - es);
+      const double yh = scale2(nyv, g - ep), xh = scale2(nrm, g - es);
       const double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
       const int en = g + protect_update(yh, tau, xh);
       sm.wsx[lane] = en - es;
@@ -434,6 +476,7 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
     // update kernel's stage layout [ntile][kc][BK/4][BN][4] ----
     if (valid && active) {
       const int sx = sm.wsx[lane];
+      const double fx = (sx >= -1022) ? pow2i(sx) : 0.0;
       const long long tstride = (long long)(2 * p.nks) * (kBN * kBK);
       double* Wc = P.W + (long long)(c / kBN) * tstride + (c % kBN) * 4;
       double* Wc1 = P.W + (long long)((c + 1) / kBN) * tstride + ((c + 1) % kBN) * 4;
@@ -443,12 +486,12 @@ __device__ void run_group(const Diag2Params& p, const Sm& sm, int nsub, const in
         if (i < len) {
           const int kr = r0 + i;
           const long long o = (long long)(kr / kBK) * (kBN * kBK) + (long long)((kr % kBK) >> 2) * (kBN * 4) + (kr & 3);
-          const double xr = ldexp(yr[i], sx);
+          const double xr = (sx >= -1022) ? yr[i] * fx : scale2_slow(yr[i], sx);
           if (!PAIR) {
             Wc[o] = -(beta * xr);
             Wc[o + half] = a * xr;
           } else {
-            const double xi = ldexp(yi[i], sx);
+            const double xi = (sx >= -1022) ? yi[i] * fx : scale2_slow(yi[i], sx);
             Wc[o] = -(beta * xr);
             Wc1[o] = -(beta * xi);
             Wc[o + half] = a * xr - b * xi;

@@ -139,6 +139,8 @@ struct Diag2Params {
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)
 cudaError_t launch_diag2(const Diag2Params& p, cudaStream_t st);
 size_t diag2_smem_bytes(int nt);
+cudaError_t launch_diag3(const Diag2Params& p, cudaStream_t st);
+size_t diag3_smem_bytes(int nt);
 cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, cudaStream_t st);
 cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int nblk,
                          const DevPlan& P, cudaStream_t st);

@@ -16,6 +16,7 @@
 // accumulators are two consecutive rows of a column of X: 16-byte loads/stores of C.
 #include <cuda.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "zz_internal.cuh"
 
@@ -74,6 +75,137 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kCWarps * 32) : "memory");
 }
 
+// v1: one CTA per (n-tile, m-tile); C loads and stores guarded by branches.
+__global__ void __launch_bounds__(kThreads, 2)
+    k_update_v1(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntile = p.ntile0 + blockIdx.x;
+  const int n0 = ntile * kBN, m0 = blockIdx.y * kBM;
+  const int nkc = 2 * p.nks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < kBN) colmax[threadIdx.x] = 0ull;
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------- producer: TMA (S/T chunks) + bulk copy (W chunk) ----------------
+    if (lane == 0) {
+      const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int s = kc % kStages;
+        if (kc >= kStages) mbar_wait(&empty[s], ((kc / kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kStageBytes);
+        const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
+        const int kcol = p.t0 + (kc % p.nks) * kBK;
+        double* a = sA + s * (kBM * kBK);
+#pragma unroll 4
+        for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
+        bulk_load(sB + s * (kBN * kBK), wt + (long long)kc * (kBN * kBK), kBBytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: 4 warps, 2 (rows) x 2 (columns), 64 x 32 each ----------------
+  const int wm = warp >> 1, wn = warp & 1;
+  const int rq = lane & 3, cq = lane >> 2;
+  double acc[4][8][2];
+  // accumulators start from the scaled pending values: 2^sY[c] * Y (exact)
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+    const int c = n0 + wn * 32 + ni * 8 + cq;
+    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
+    const bool ld = cvalid && (c >= p.first_end);
+    const int sy = ld ? p.sY[c] : 0;
+    const double* xc = p.X + (long long)c * p.ldx;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      double v0 = 0.0, v1 = 0.0;
+      if (ld && i0 < p.rows) {
+        if (p.vec && i0 + 1 < p.rows) {
+          double2 t = *reinterpret_cast<const double2*>(xc + i0);
+          v0 = t.x; v1 = t.y;
+        } else {
+          v0 = xc[i0];
+          if (i0 + 1 < p.rows) v1 = xc[i0 + 1];
+        }
+        if (sy != 0) { v0 = ldexp(v0, sy); v1 = ldexp(v1, sy); }
+      }
+      acc[ni][mi][0] = v0;
+      acc[ni][mi][1] = v1;
+    }
+  }
+
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int s = kc % kStages;
+    mbar_wait(&full[s], (kc / kStages) & 1);
+    const double* a = sA + s * (kBM * kBK);
+    const double* b = sB + s * (kBN * kBK);
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      double fw[4], fs[8];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wn * 32 + ni * 8 + cq) * 4 + rq];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+    const int c = n0 + wn * 32 + ni * 8 + cq;
+    const bool cvalid = (c >= p.c_begin) && (c < p.n_sel);
+    double* xc = p.X + (long long)c * p.ldx;
+    double cm = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
+      if (cvalid && i0 < p.rows) {
+        if (p.vec && i0 + 1 < p.rows) {
+          *reinterpret_cast<double2*>(xc + i0) = make_double2(v0, v1);
+        } else {
+          xc[i0] = v0;
+          if (i0 + 1 < p.rows) xc[i0 + 1] = v1;
+        }
+      }
+      if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
+      if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
+    }
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+    if (rq == 0 && cvalid && cm > 0.0)
+      atomicMax(&colmax[c - n0], (unsigned long long)__double_as_longlong(cm));
+  }
+  consumer_sync();
+  if (threadIdx.x < kBN) {
+    const int c = n0 + threadIdx.x;
+    const unsigned long long v = colmax[threadIdx.x];
+    if (v != 0ull && c >= p.c_begin && c < p.n_sel) atomicMax(&p.nY_out[c], v);
+  }
+}
+
 // predicated global accesses (no branch around a load: every C load of a lane is issued
 // before the first one is consumed)
 __device__ __forceinline__ void ld2p(double& x, double& y, const double* p, bool pr) {
@@ -100,7 +232,7 @@ __device__ __forceinline__ void ld1p_i(int& x, const int* p, bool pr) {
 // warp runs ahead into the next tile while the consumers finish the current epilogue.
 __global__ void __maxnreg__(200)
     k_update(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
-             int n_mtiles, int n_tiles) {
+             int n_mtiles, int n_tiles, int m_fast) {
   extern __shared__ __align__(1024) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
@@ -126,8 +258,9 @@ __global__ void __maxnreg__(200)
     if (lane == 0) {
       int g = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile % n_mtiles) * kBM;
-        const int ntile = p.ntile0 + tile / n_mtiles;
+        const int n_ntl = n_tiles / n_mtiles;
+        const int m0 = (m_fast ? tile % n_mtiles : tile / n_ntl) * kBM;
+        const int ntile = p.ntile0 + (m_fast ? tile / n_mtiles : tile % n_ntl);
         const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
         for (int kc = 0; kc < nkc; ++kc, ++g) {
           const int s = g % kStages;
@@ -150,8 +283,9 @@ __global__ void __maxnreg__(200)
   const int rq = lane & 3, cq = lane >> 2;
   int g = 0;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int m0 = (tile % n_mtiles) * kBM;
-    const int n0 = (p.ntile0 + tile / n_mtiles) * kBN;
+    const int n_ntl = n_tiles / n_mtiles;
+    const int m0 = (m_fast ? tile % n_mtiles : tile / n_ntl) * kBM;
+    const int n0 = (p.ntile0 + (m_fast ? tile / n_mtiles : tile % n_ntl)) * kBN;
     double acc[4][8][2];
     // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
     int sy[4];
@@ -244,8 +378,16 @@ static int g_upd_sms = 0;
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st) {
   static bool attr = false;
+  static const int ver = getenv("ZZ_UPD") ? atoi(getenv("ZZ_UPD")) : 1;
   if (!attr) {
+    cudaError_t e1 = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e1 != cudaSuccess) return e1;
+    e1 = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e1 != cudaSuccess) return e1;
     cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    // two CTAs per SM need the maximum shared-memory carve-out (2 x 99 KB)
+    e = cudaFuncSetAttribute(k_update, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     int dev;
     cudaGetDevice(&dev);
@@ -253,9 +395,19 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
+  if (ver == 1) {
+    dim3 g1(n_ntiles, n_mtiles);
+    k_update_v1<<<g1, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
+    return cudaGetLastError();
+  }
+  // ZZ_UPD_PERSIST=k: k CTAs per SM walk the tiles (0: one CTA per tile); ZZ_UPD_MFAST=1:
+  // consecutive tiles share an N tile (development switches, measured in profiles/)
+  static const int persist = getenv("ZZ_UPD_PERSIST") ? atoi(getenv("ZZ_UPD_PERSIST")) : 0;
+  static const int m_fast = getenv("ZZ_UPD_MFAST") ? atoi(getenv("ZZ_UPD_MFAST")) : 0;
   const int n_tiles = n_mtiles * n_ntiles;
-  const int grid = n_tiles < 2 * g_upd_sms ? n_tiles : 2 * g_upd_sms;
-  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
+  int grid = n_tiles;
+  if (persist > 0 && grid > persist * g_upd_sms) grid = persist * g_upd_sms;
+  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles, m_fast);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
 """Development check: thread-per-eigenvector diagonal solve (default) vs the warp-per-column
-kernel (ZZ_DIAG_WARP=1, run in a subprocess) vs the oracle; prints parity and timings."""
+kernel (ZZ_DIAG=1, run in a subprocess) vs the oracle; prints parity and timings."""
 import json
 import os
 import subprocess
@@ -51,8 +51,7 @@ if __name__ == "__main__":
         res = {}
         for mode in ("new", "warp"):
             env = dict(os.environ)
-            if mode == "warp":
-                env["ZZ_DIAG_WARP"] = "1"
+            env["ZZ_DIAG"] = "1" if mode == "warp" else os.environ.get("ZZ_DIAG", "3")
             out = "/tmp/cmp_%s_%s.npy" % (name, mode)
             r = subprocess.run([sys.executable, __file__, "child", name, str(seed), str(mb), out], env=env,
                                capture_output=True, text=True)
