@@ -136,7 +136,7 @@ int make_map(Context* c, CUtensorMap* tm, const double* A, long long lda, int m)
   }
   cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)m};
   cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
-  cuuint32_t box[2] = {8, (cuuint32_t)kBK};
+  cuuint32_t box[2] = {(cuuint32_t)update_box_rows(), (cuuint32_t)kBK};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = c->encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -311,23 +311,26 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       const double xn = two ? dmaxd(nmax(xt), nmax(xb)) : nmax(xb);
       // in-block update of the block rows above js (ProtectUpdate)
       if (js > s0) {
-        double tt = 0.0;
-        for (int kk = js; kk <= j; ++kk) {
-          const double2 cmv = sm.cm[kk];
-          tt = __dadd_rn(tt, __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y)));
+        // bound of the rows above the block rows js..j: their in-tile column bounds (R6)
+        const double2 cmv = sm.cm[j];
+        const double tt = __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y));
+        // fast path: bound + tt xn <= 2^1020 implies ProtectUpdate(bound, tt, xn) = 0
+        double nb = fma(tt, xn, bound);
+        if (__any_sync(0xffffffffu, !(nb <= 0x1p1020))) {
+          // exact maximum of the pending rows, then ProtectUpdate (warp-uniform: shuffles)
+          bound = pending_max<G, PAIR>(s, rot, t, js);
+          const int eu = protect_update(bound, tt, xn);
+          if (eu < 0) {
+            s.scale(eu);
+            ex += eu;
+            bound = scale2k(bound, eu);
+            xnb = scale2k(xnb, eu);
+            xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
+            xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
+          }
+          nb = __dadd_rn(bound, __dmul_rn(tt, xn));
         }
-        // exact maximum when the running bound would scale (warp-uniform: it shuffles)
-        if (__any_sync(0xffffffffu, protect_update(bound, tt, xn) < 0)) bound = pending_max<G, PAIR>(s, rot, t, js);
-        const int eu = protect_update(bound, tt, xn);
-        if (eu < 0) {
-          s.scale(eu);
-          ex += eu;
-          bound = scale2k(bound, eu);
-          xnb = scale2k(xnb, eu);
-          xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
-          xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
-        }
-        bound = __dadd_rn(bound, __dmul_rn(tt, xn));
+        bound = nb;
         // sources in ascending row order, as the oracle's O6
 #pragma unroll
         for (int sidx = 0; sidx < 2; ++sidx) {
@@ -364,15 +367,19 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       // ---- update of all rows above the block by DMMA (Alg. 3 on the in-tile panel) ----
       const double2 tv = sm.tau[blk];
       const double tt = __dadd_rn(__dmul_rn(beta, tv.x), __dmul_rn(ab, tv.y));
-      if (__any_sync(0xffffffffu, protect_update(bound, tt, xnb) < 0)) bound = pending_max<G, PAIR>(s, rot, t, s0);
-      const int eu = protect_update(bound, tt, xnb);
-      if (eu < 0) {
-        s.scale(eu);
-        ex += eu;
-        bound = scale2k(bound, eu);
-        xnb = scale2k(xnb, eu);
+      double nb = fma(tt, xnb, bound);
+      if (__any_sync(0xffffffffu, !(nb <= 0x1p1020))) {
+        bound = pending_max<G, PAIR>(s, rot, t, s0);
+        const int eu = protect_update(bound, tt, xnb);
+        if (eu < 0) {
+          s.scale(eu);
+          ex += eu;
+          bound = scale2k(bound, eu);
+          xnb = scale2k(xnb, eu);
+        }
+        nb = __dadd_rn(bound, __dmul_rn(tt, xnb));
       }
-      bound = __dadd_rn(bound, __dmul_rn(tt, xnb));
+      bound = nb;
       // A fragments: lane (team, t) holds its column's coefficient for source row src0 + t;
       // the value of row 8 blk + r lives on lane r >> 1 of the team (register r & 1).
       double aS[3], aT[3];
@@ -545,6 +552,15 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
     }
     sm.cm[j] = make_double2(ms, mt);
   }
+  __syncthreads();
+  // a 2x2 block's bottom row carries the bound of both of its source columns (one row per
+  // thread: blockDim >= kDiag2MaxNT >= nt)
+  double2 cm2 = make_double2(0.0, 0.0);
+  for (int j = threadIdx.x; j < nt; j += blockDim.x)
+    if (sm.fl[j] == kRowBot2) cm2 = make_double2(sm.cm[j - 1].x + sm.cm[j].x, sm.cm[j - 1].y + sm.cm[j].y);
+  __syncthreads();
+  for (int j = threadIdx.x; j < nt; j += blockDim.x)
+    if (sm.fl[j] == kRowBot2) sm.cm[j] = cm2;
   __syncthreads();
   // block panel norms: max over rows above the block of the row sums over its rows
   for (int b = warp; b < nblk; b += kW3) {

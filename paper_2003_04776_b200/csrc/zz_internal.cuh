@@ -110,6 +110,7 @@ struct UpdParams {
   int first_end;     // columns < first_end start from C = 0 (cs_{I+1})
   int n_sel;
   int ntile0;        // first N tile index (c_begin / BN)
+  int ntile_end;     // one past the last 64-column N tile (set by the launcher)
   double* X; long long ldx;
   const double* W;
   const int* sY;
@@ -158,5 +159,7 @@ cudaError_t launch_normalize(int m, int n_sel, int M, double* X, long long ldx, 
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st);
 size_t diag_smem_bytes(int nt);
+int update_version();
+int update_box_rows();   // rows per TMA box of the S/T tensor maps
 
 }  // namespace zz

@@ -230,62 +230,81 @@ __device__ __forceinline__ void ld1p_i(int& x, const int* p, bool pr) {
 
 // Persistent: each CTA walks the (m-tile, n-tile) grid with stride gridDim.x; the producer
 // warp runs ahead into the next tile while the consumers finish the current epilogue.
-__global__ void __maxnreg__(200)
-    k_update(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
-             int n_mtiles, int n_tiles, int m_fast) {
+// WN column warps x 2 row warps consume a 128 x (32 WN) tile; WN = 4 is one 288-thread CTA
+// per SM sharing each S/T stage between 128 columns (half the A traffic of WN = 2).
+template <int WN, int BOX = 8>
+struct UT {
+  static constexpr int BN = 32 * WN;
+  static constexpr int CW = 2 * WN;                         // consumer warps
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int BBYTES = BN * kBK * 8;               // W chunk: BN/64 blocks [BK/4][64][4]
+  static constexpr int STAGE = kABytes + BBYTES;
+  static constexpr int SMEM = kStages * STAGE + 2 * kStages * 8 + BN * 8;
+  static constexpr int MINB = (WN == 2) ? 2 : 1;
+};
+
+template <int WN, int BOX>
+__global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
+    k_update_t(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
+               int n_mtiles, int n_tiles) {
+  using C = UT<WN, BOX>;
   extern __shared__ __align__(1024) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE);
   uint64_t* empty = full + kStages;
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkc = 2 * p.nks;
+  const int n_ntl = n_tiles / n_mtiles;
+  // W is stored per 64-column block: [ntile64][kc][BK/4][64][4]
+  const long long wtile = (long long)nkc * (kBN * kBK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCWarps);
+      mbar_init(&empty[s], C::CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x < kBN) colmax[threadIdx.x] = 0ull;
+  if (threadIdx.x < C::BN) colmax[threadIdx.x] = 0ull;
   __syncthreads();
 
-  if (warp == kCWarps) {
-    // ---------------- producer: TMA (S/T chunks) + bulk copy (W chunk) ----------------
+  if (warp == C::CW) {
+    // ---------------- producer: TMA (S/T chunks) + bulk copies (W chunk) ----------------
     if (lane == 0) {
       int g = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int n_ntl = n_tiles / n_mtiles;
-        const int m0 = (m_fast ? tile % n_mtiles : tile / n_ntl) * kBM;
-        const int ntile = p.ntile0 + (m_fast ? tile / n_mtiles : tile % n_ntl);
-        const double* wt = p.W + (long long)ntile * nkc * (kBN * kBK);
+        const int m0 = (tile / n_ntl) * kBM;
+        const int nb64 = p.ntile0 + (tile % n_ntl) * (C::BN / kBN);   // first 64-column block
+        const int nblk = min(C::BN / kBN, p.ntile_end - nb64);         // 64-column blocks present
         for (int kc = 0; kc < nkc; ++kc, ++g) {
           const int s = g % kStages;
           if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
-          mbar_expect_tx(&full[s], kStageBytes);
+          mbar_expect_tx(&full[s], kABytes + nblk * kBBytes);
           const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
           const int kcol = p.t0 + (kc % p.nks) * kBK;
           double* a = sA + s * (kBM * kBK);
+          // S/T chunk as [BM/BOX][BK][BOX] (BOX = 4: conflict-free fragment loads)
 #pragma unroll 4
-          for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
-          bulk_load(sB + s * (kBN * kBK), wt + (long long)kc * (kBN * kBK), kBBytes, &full[s]);
+          for (int mo = 0; mo < kBM / BOX; ++mo) tma_load_2d(a + mo * (kBK * BOX), tm, m0 + mo * BOX, kcol, &full[s]);
+          for (int q = 0; q < nblk; ++q)
+            bulk_load(sB + s * (C::BN * kBK) + q * (kBN * kBK), p.W + (long long)(nb64 + q) * wtile + (long long)kc * (kBN * kBK),
+                      kBBytes, &full[s]);
         }
       }
     }
     return;
   }
 
-  // ---------------- consumers: 4 warps, 2 (rows) x 2 (columns), 64 x 32 each ----------------
-  const int wm = warp >> 1, wn = warp & 1;
+  // ---------------- consumers: 2 (rows) x WN (columns) warps, 64 x 32 each ----------------
+  const int wm = warp / WN, wn = warp % WN;
   const int rq = lane & 3, cq = lane >> 2;
   int g = 0;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int n_ntl = n_tiles / n_mtiles;
-    const int m0 = (m_fast ? tile % n_mtiles : tile / n_ntl) * kBM;
-    const int n0 = (p.ntile0 + (m_fast ? tile / n_mtiles : tile % n_ntl)) * kBN;
+    const int m0 = (tile / n_ntl) * kBM;
+    const int n0 = (p.ntile0 + (tile % n_ntl) * (C::BN / kBN)) * kBN;
     double acc[4][8][2];
     // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
     int sy[4];
@@ -317,19 +336,27 @@ __global__ void __maxnreg__(200)
         }
       }
     }
-
+    const double* bw = sB + (wn >> 1) * (kBN * kBK);   // this warp's 64-column block of W
+    const int wc = (wn & 1) * 32;
     for (int kc = 0; kc < nkc; ++kc, ++g) {
       const int s = g % kStages;
       mbar_wait(&full[s], (g / kStages) & 1);
       const double* a = sA + s * (kBM * kBK);
-      const double* b = sB + s * (kBN * kBK);
+      const double* b = bw + s * (C::BN * kBK);
 #pragma unroll
       for (int ks = 0; ks < kBK / 4; ++ks) {
         double fw[4], fs[8];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wn * 32 + ni * 8 + cq) * 4 + rq];
+        for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wc + ni * 8 + cq) * 4 + rq];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+        for (int mi = 0; mi < 8; ++mi) {
+          if (BOX == 8) {
+            fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+          } else {
+            const int grp = wm * 16 + mi * 2 + (cq >> 2);
+            fs[mi] = a[(grp * kBK + ks * 4 + rq) * 4 + (cq & 3)];
+          }
+        }
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -362,32 +389,60 @@ __global__ void __maxnreg__(200)
       if (rq == 0 && cvalid && cm > 0.0)
         atomicMax(&colmax[c - n0], (unsigned long long)__double_as_longlong(cm));
     }
-    consumer_sync();
-    if (threadIdx.x < kBN) {
+    asm volatile("bar.sync 1, %0;" ::"n"(C::CW * 32) : "memory");
+    if (threadIdx.x < C::BN) {
       const int c = n0 + threadIdx.x;
       const unsigned long long v = colmax[threadIdx.x];
       if (v != 0ull && c >= p.c_begin && c < p.n_sel) atomicMax(&p.nY_out[c], v);
       colmax[threadIdx.x] = 0ull;
     }
-    consumer_sync();
+    asm volatile("bar.sync 1, %0;" ::"n"(C::CW * 32) : "memory");
   }
 }
 
 static int g_upd_sms = 0;
 
+int update_version() {
+  static const int ver = getenv("ZZ_UPD") ? atoi(getenv("ZZ_UPD")) : 2;
+  return ver;
+}
+int update_box_rows() { return update_version() == 3 ? 4 : 8; }
+
+template <int WN, int BOX>
+static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
+                            cudaStream_t st, int persist) {
+  using C = UT<WN, BOX>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_update_t<WN, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_update_t<WN, BOX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int per = C::BN / kBN;
+  const int n_ntl = (n_ntiles64 + per - 1) / per;
+  p.ntile_end = p.ntile0 + n_ntiles64;
+  const int n_tiles = n_mtiles * n_ntl;
+  int grid = n_tiles;
+  if (persist > 0 && grid > persist * g_upd_sms) grid = persist * g_upd_sms;
+  k_update_t<WN, BOX><<<grid, C::THREADS, C::SMEM, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st) {
+  // ZZ_UPD: 2 (default) = 128 x 64 tiles, 2 CTAs per SM, batched predicated C loads;
+  // 3 = the same with 4-row TMA boxes (conflict-free S/T fragment loads); 4 = 128 x 128
+  // tiles with 8 consumer warps (1 CTA per SM); 1 = the first version (branchy C loads).
+  // ZZ_UPD_PERSIST=k: k CTAs per SM walk the tiles.  (Variants are measured in profiles/.)
+  const int ver = update_version();
+  static const int persist = getenv("ZZ_UPD_PERSIST") ? atoi(getenv("ZZ_UPD_PERSIST")) : 0;
   static bool attr = false;
-  static const int ver = getenv("ZZ_UPD") ? atoi(getenv("ZZ_UPD")) : 1;
   if (!attr) {
-    cudaError_t e1 = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e1 != cudaSuccess) return e1;
-    e1 = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e1 != cudaSuccess) return e1;
-    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
-    // two CTAs per SM need the maximum shared-memory carve-out (2 x 99 KB)
-    e = cudaFuncSetAttribute(k_update, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(k_update_v1, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     int dev;
     cudaGetDevice(&dev);
@@ -395,19 +450,11 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
-  if (ver == 1) {
-    dim3 g1(n_ntiles, n_mtiles);
-    k_update_v1<<<g1, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
-    return cudaGetLastError();
-  }
-  // ZZ_UPD_PERSIST=k: k CTAs per SM walk the tiles (0: one CTA per tile); ZZ_UPD_MFAST=1:
-  // consecutive tiles share an N tile (development switches, measured in profiles/)
-  static const int persist = getenv("ZZ_UPD_PERSIST") ? atoi(getenv("ZZ_UPD_PERSIST")) : 0;
-  static const int m_fast = getenv("ZZ_UPD_MFAST") ? atoi(getenv("ZZ_UPD_MFAST")) : 0;
-  const int n_tiles = n_mtiles * n_ntiles;
-  int grid = n_tiles;
-  if (persist > 0 && grid > persist * g_upd_sms) grid = persist * g_upd_sms;
-  k_update<<<grid, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles, m_fast);
+  if (ver == 2) return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 3) return launch_t<2, 4>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 4) return launch_t<4, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  dim3 g1(n_ntiles, n_mtiles);
+  k_update_v1<<<g1, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
   return cudaGetLastError();
 }
 
