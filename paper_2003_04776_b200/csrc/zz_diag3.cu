@@ -57,13 +57,14 @@ struct Sm3 {
   double2* cm;     // per row j: max |S_ij|, |T_ij| over the tile rows above j's block (R6)
   double2* tau;    // per block b: max over rows i < s_b of the sums over the block's rows
   int* bs;         // block b = rows [bs[b], bs[b+1]); bs[b] = 8b - (row 8b is a 2x2 bottom)
+  double* slab;    // per warp: the current block's rows, [9 slots][8 columns]
   signed char* fl; // row flags
 };
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ __forceinline__ size_t smem3(int nt) {
   return a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3)) + a16(sizeof(double2) * (size_t)nt) +
-         a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16((size_t)nt);
+         a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(sizeof(double) * 16 * 72) + a16((size_t)nt);
 }
 __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt) {
   Sm3 s;
@@ -72,6 +73,7 @@ __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt) {
   s.cm = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * (size_t)nt);
   s.tau = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * 17);
   s.bs = reinterpret_cast<int*>(base + o); o += a16(sizeof(int) * 18);
+  s.slab = reinterpret_cast<double*>(base + o); o += a16(sizeof(double) * 16 * 72);
   s.fl = reinterpret_cast<signed char*>(base + o);
   return s;
 }
@@ -208,7 +210,7 @@ __device__ __forceinline__ double pending_max(const Seg<G>& s, int rot, int t, i
 // One task: 8 real columns (PAIR = false) or 4 complex pairs (PAIR = true) of tile I.
 // ------------------------------------------------------------------------------------
 template <int G, bool PAIR>
-__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane) {
+__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, double* wslab) {
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
@@ -255,40 +257,42 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     const bool st = s0 < g8;             // row 8 blk - 1 (a 2x2 top) belongs to this block
     double xnb = 0.0;                    // max |x| over the block's solved rows
     // ---- bottom-up substitution inside the block ----
+    // The block's rows go to a per-warp shared-memory slab (slot q = row 8 blk - 1 + q; slot
+    // 0 is the top of a straddling 2x2 block; entry [q][team] = this column's value) where
+    // the row loop indexes them at run time.  All 4 lanes of a column (and both columns of
+    // a pair) compute identical values, hence identical decisions, and store identical
+    // values.
+    __syncwarp();
+    wslab[(1 + 2 * t) * 8 + team] = s.y[CUR][0];
+    wslab[(2 + 2 * t) * 8 + team] = s.y[CUR][1];
+    if (t == 3) wslab[team] = s.y[PRV][1];
+    __syncwarp();
+    const int q0 = s0 - (g8 - 1);
     int j = e0 - 1;
     while (j >= s0) {
+      const int q = j - (g8 - 1);
       const bool two = sm.fl[j] == kRowBot2;
-      const int js = two ? j - 1 : j;
-      // the right-hand side values of rows j (and j-1) from their owner lanes
-      const int jb = j - g8, jt = j - 1 - g8;
-      double vb = (jb & 1) ? s.y[CUR][1] : s.y[CUR][0];
-      vb = __shfl_sync(0xffffffffu, vb, pbase + (jb >> 1));
-      double vt = 0.0;
-      if (two) {
-        vt = (jt >= 0) ? ((jt & 1) ? s.y[CUR][1] : s.y[CUR][0]) : s.y[PRV][1];
-        vt = __shfl_sync(0xffffffffu, vt, pbase + ((jt >= 0) ? (jt >> 1) : 3));
-      }
+      const int qs = two ? q - 1 : q;
+      const int pt = PAIR ? (team & ~1) : team;     // (Re, Im) entries of the pair
       int k = 0;
       cpx xt, xb;
       {
-        const double ob = PAIR ? __shfl_xor_sync(0xffffffffu, vb, 4) : 0.0;
-        const double ot = PAIR ? __shfl_xor_sync(0xffffffffu, vt, 4) : 0.0;
-        cpx wb = PAIR ? (comp ? mkc(ob, vb) : mkc(vb, ob)) : mkc(vb, 0.0);
-        cpx wt = PAIR ? (comp ? mkc(ot, vt) : mkc(vt, ot)) : mkc(vt, 0.0);
+        cpx wb = mkc(wslab[q * 8 + pt], PAIR ? wslab[q * 8 + pt + 1] : 0.0);
         if (two) {
+          cpx wt = mkc(wslab[(q - 1) * 8 + pt], PAIR ? wslab[(q - 1) * 8 + pt + 1] : 0.0);
           const double2 d11 = sm.ST[poff3(j - 1) + j - 1], d21 = sm.ST[poff3(j - 1) + j];
           const double2 d12 = sm.ST[poff3(j) + j - 1], d22 = sm.ST[poff3(j) + j];
           solve2x2<PAIR>(wt, wb, d11.x, d21.x, d12.x, d22.x, d11.y, d12.y, d22.y, a, b, beta, ab, k);
           if (PAIR && tip && tipr == j) {
             // tip of a complex pair (reading R10): rows (r-1, r) of the eigenvalue block
             const double pp = __dmul_rn(beta, d21.x);
-            const cpx q = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
-            if (fabs(pp) >= n1(q)) {
+            const cpx qq = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
+            if (fabs(pp) >= n1(qq)) {
               wb = mkc(1.0, 0.0);
-              wt = mkc(__ddiv_rn(-q.re, pp), __ddiv_rn(-q.im, pp));
+              wt = mkc(__ddiv_rn(-qq.re, pp), __ddiv_rn(-qq.im, pp));
             } else {
               wt = mkc(1.0, 0.0);
-              const cpx z = cdivx(mkc(pp, 0.0), q);
+              const cpx z = cdivx(mkc(pp, 0.0), qq);
               wb = mkc(-z.re, -z.im);
             }
             k = 0;
@@ -302,67 +306,73 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
           xt = xb;
         }
       }
+      // scalars follow the solve's scaling at once; the stored values once (below)
       if (k < 0) {
-        s.scale(k);
-        ex += k;
         bound = scale2k(bound, k);
         xnb = scale2k(xnb, k);
       }
-      const double xn = two ? dmaxd(nmax(xt), nmax(xb)) : nmax(xb);
-      // in-block update of the block rows above js (ProtectUpdate)
-      if (js > s0) {
-        // bound of the rows above the block rows js..j: their in-tile column bounds (R6)
+      double xn = two ? dmaxd(nmax(xt), nmax(xb)) : nmax(xb);
+      int eu = 0;
+      double tt = 0.0;
+      const bool upd = qs > q0;
+      if (upd) {
+        // in-block update of the block rows above (ProtectUpdate) against a running
+        // upper bound of the pending rows; lane-local (every lane holds the same values)
         const double2 cmv = sm.cm[j];
-        const double tt = __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y));
-        // fast path: bound + tt xn <= 2^1020 implies ProtectUpdate(bound, tt, xn) = 0
+        tt = __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y));
         double nb = fma(tt, xn, bound);
-        if (__any_sync(0xffffffffu, !(nb <= 0x1p1020))) {
-          // exact maximum of the pending rows, then ProtectUpdate (warp-uniform: shuffles)
-          bound = pending_max<G, PAIR>(s, rot, t, js);
-          const int eu = protect_update(bound, tt, xn);
-          if (eu < 0) {
-            s.scale(eu);
-            ex += eu;
-            bound = scale2k(bound, eu);
-            xnb = scale2k(xnb, eu);
-            xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
-            xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
-          }
-          nb = __dadd_rn(bound, __dmul_rn(tt, xn));
+        if (!(nb <= 0x1p1020)) {
+          eu = protect_update(bound, tt, xn);
+          nb = __dadd_rn(scale2k(bound, eu), __dmul_rn(tt, scale2k(xn, eu)));
         }
         bound = nb;
-        // sources in ascending row order, as the oracle's O6
+      }
+      if (k + eu < 0) {
+        // the whole segment by 2^(k+eu): pending rows in registers, the block's rows in the slab
+        const int kk = k + eu;
+        s.scale(kk);
+        __syncwarp();
+        for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], kk);
+        __syncwarp();
+        ex += kk;
+        if (eu < 0) {
+          xnb = scale2k(xnb, eu);
+          xn = scale2k(xn, eu);
+          xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
+          xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
+        }
+      }
+      xnb = dmaxd(xnb, xn);
+      if (upd) {
+        // sources in ascending row order, as the oracle's O6; each lane updates the rows of
+        // its column (4 lanes split the rows)
 #pragma unroll
         for (int sidx = 0; sidx < 2; ++sidx) {
           if (sidx == 0 && !two) continue;
           const cpx x = sidx ? xb : xt;
-          const int src = sidx ? j : js;
           const double xo = PAIR ? (comp ? x.im : x.re) : x.re;
           const double ur = beta * xo;
           const double wr = PAIR ? (comp ? (a * x.im + b * x.re) : (a * x.re - b * x.im)) : a * x.re;
-          const double2* col = sm.ST + poff3(src);
-          const int r0 = g8 + 2 * t;
-          if (r0 < js) { const double2 v = col[r0]; s.y[CUR][0] = fma(v.y, wr, fma(-v.x, ur, s.y[CUR][0])); }
-          if (r0 + 1 < js) { const double2 v = col[r0 + 1]; s.y[CUR][1] = fma(v.y, wr, fma(-v.x, ur, s.y[CUR][1])); }
-          if (st && t == 3 && g8 - 1 < js) {
-            const double2 v = col[g8 - 1];
-            s.y[PRV][1] = fma(v.y, wr, fma(-v.x, ur, s.y[PRV][1]));
+          const double2* col = sm.ST + poff3(sidx ? j : j - 1) + (g8 - 1);
+          for (int r = q0 + t; r < qs; r += 4) {
+            const double2 v = col[r];
+            wslab[r * 8 + team] = fma(v.y, wr, fma(-v.x, ur, wslab[r * 8 + team]));
           }
         }
       }
-      xnb = dmaxd(xnb, xn);
-      // owners store the solution
-      {
-        const double ob = PAIR ? (comp ? xb.im : xb.re) : xb.re;
-        const double ot = PAIR ? (comp ? xt.im : xt.re) : xt.re;
-        if (t == (jb >> 1)) { if (jb & 1) s.y[CUR][1] = ob; else s.y[CUR][0] = ob; }
-        if (two) {
-          if (jt >= 0) { if (t == (jt >> 1)) { if (jt & 1) s.y[CUR][1] = ot; else s.y[CUR][0] = ot; } }
-          else if (t == 3) s.y[PRV][1] = ot;
-        }
+      // the solution into the slab (own component)
+      if (t == 0) {
+        wslab[q * 8 + team] = PAIR ? (comp ? xb.im : xb.re) : xb.re;
+        if (two) wslab[(q - 1) * 8 + team] = PAIR ? (comp ? xt.im : xt.re) : xt.re;
       }
-      j = js - 1;
+      __syncwarp();
+      j = qs - 1 + (g8 - 1);
     }
+    // ---- the block's rows back to their owner lanes ----
+    s.y[CUR][0] = wslab[(1 + 2 * t) * 8 + team];
+    s.y[CUR][1] = wslab[(2 + 2 * t) * 8 + team];
+    if (st && t == 3) s.y[PRV][1] = wslab[team];
+    __syncwarp();
     if (blk > 0) {
       // ---- update of all rows above the block by DMMA (Alg. 3 on the in-tile panel) ----
       const double2 tv = sm.tau[blk];
@@ -587,8 +597,8 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   const int npt = (p.n_pair + 3) / 4, nrt = (p.n_real + 7) / 8;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two
   for (int task = warp * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * kW3) {
-    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane);
-    else solve_task<G, false>(p, sm, nblk, task - npt, lane);
+    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, sm.slab + warp * 72);
+    else solve_task<G, false>(p, sm, nblk, task - npt, lane, sm.slab + warp * 72);
   }
 }
 

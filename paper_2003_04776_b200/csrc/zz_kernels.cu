@@ -544,7 +544,9 @@ __device__ void solve_item(const DiagParams& p, const Tile& tl, int c, int lane)
   if (!p.do_update) return;
   // scaling decision of the update at this step (Alg. 3 P:253-259 with Alg. 2 P:228-232;
   // reading R5): align to gamma = min exponent, then ProtectUpdate.
+  // pending max of the column (a pair: of both of its columns)
   double nyv = tip ? 0.0 : __longlong_as_double((long long)P.nY[(long long)p.nY_in * p.n_sel + c]);
+  if (PAIR && !tip) nyv = dmaxd(nyv, __longlong_as_double((long long)P.nY[(long long)p.nY_in * p.n_sel + c + 1]));
   int g = min(ep, es);
   double yh = ldexp(nyv, g - ep), xh = ldexp(nrm, g - es);
   double tau = __dadd_rn(__dmul_rn(beta, p.P.cS[p.I]), __dmul_rn(ab, p.P.cT[p.I]));
