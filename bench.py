@@ -312,9 +312,16 @@ def main():
     upd_avg = upd_ms / max(1, args.steps * max(1, len(per_launch)))
     if upd_ms > 0:
         ach = (F_upd / len(per_launch)) / (upd_avg * 1e-3) * 1e-12
+        traffic, tnote = None, None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_update"]
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            tnote = "DRAM bytes of one k_update launch, " + tr["source"]
+        except Exception:
+            pass
         res["roofline"] = {"bound": "tensor", "kernel": "k_update (DMMA.8x8x4 FP64 contraction)",
                            "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
-                           "traffic": None, "peak_source": PEAK_SRC,
+                           "traffic": traffic, "traffic_note": tnote, "peak_source": PEAK_SRC,
                            "algorithmic_flops_per_launch": F_upd / len(per_launch),
                            "avg_launch_ms": upd_avg,
                            "share_of_step": upd_ms / args.steps / (t * 1e3)}

@@ -252,9 +252,13 @@ def tgevc_host(S, T, select=None, X=None, col_scale_exp=None, device=None):
         if hasattr(A, "data_ptr"):
             return A.data_ptr(), _ld_colmajor(A, m, what)
         A = np.asarray(A)
-        if not A.flags.f_contiguous or A.dtype != np.float64:
-            raise ValueError("%s must be a Fortran-ordered float64 array" % what)
-        return A.ctypes.data, max(m, 1)
+        if A.dtype != np.float64 or A.ndim != 2 or A.shape[0] != m:
+            raise ValueError("%s must be a float64 array with %d rows" % (what, m))
+        if A.shape[1] <= 1 or A.flags.f_contiguous:
+            return A.ctypes.data, max(m, 1)
+        if A.strides[0] != 8 or A.strides[1] % 8:
+            raise ValueError("%s must be column-major (element (i,j) at i + j*ld)" % what)
+        return A.ctypes.data, A.strides[1] // 8
 
     sel = _sel_array(select, m)
     ps, lds = ptr_ld(S, "S")

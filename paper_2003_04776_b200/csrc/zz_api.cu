@@ -61,6 +61,9 @@ struct Context {
   Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev_copy;       // per-panel arrival events of zz_tgevc_host
+  cudaStream_t copy = nullptr;            // host-to-device copy stream of zz_tgevc_host
+  cudaEvent_t e_copy = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   ~Context() {}
   void release() {
@@ -69,6 +72,12 @@ struct Context {
     for (Buf* b : all) b->release();
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
+    for (cudaEvent_t e : ev_copy) cudaEventDestroy(e);
+    ev_copy.clear();
+    if (copy) cudaStreamDestroy(copy);
+    copy = nullptr;
+    if (e_copy) cudaEventDestroy(e_copy);
+    e_copy = nullptr;
     if (e0) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); }
     e0 = e1 = e2 = e3 = nullptr;
   }
@@ -144,9 +153,21 @@ int make_map(Context* c, CUtensorMap* tm, const double* A, long long lda, int m)
   return r == CUDA_SUCCESS ? 0 : ZZ_ERR_CUDA;
 }
 
+// zz_tgevc_host: S and T arrive from host memory panel by panel, in the order the wavefront
+// consumes them (tile columns M-1 .. 0, upper part and subdiagonal only), on a copy stream;
+// step I waits for panel I only, so the copies overlap the solve.
+struct HostStage {
+  const double* Sh;
+  long long ldsh;
+  const double* Th;
+  long long ldth;
+  cudaStream_t copy;
+  std::vector<cudaEvent_t>* ev;
+};
+
 // The solve on device pointers.  S/T are const; X, cse written.
 int tgevc_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
-                 const int* select, double* X, long long ldx, int* cse) {
+                 const int* select, double* X, long long ldx, int* cse, const HostStage* hs = nullptr) {
   cudaStream_t st = c->stream;
   zz_info_t info;
   memset(&info, 0, sizeof(info));
@@ -158,13 +179,17 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   }
   CK(cudaEventRecord(c->e0, st));
   int launches = 0;
-  // ---- a1: structure scan (one host sync) ----
-  CK(c->sub.ensure(sizeof(double) * (size_t)std::max(m, 1)));
-  CK(launch_subdiag(S, lds, m, c->sub.as<double>(), st));
-  launches += (m > 1);
+  // ---- a1: structure scan (one host sync; none when S is on the host) ----
   std::vector<double> sub((size_t)std::max(m - 1, 1), 0.0);
-  if (m > 1) CK(cudaMemcpyAsync(sub.data(), c->sub.p, sizeof(double) * (m - 1), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (hs) {
+    for (int j = 0; j + 1 < m; ++j) sub[j] = hs->Sh[(size_t)j * hs->ldsh + j + 1];
+  } else {
+    CK(c->sub.ensure(sizeof(double) * (size_t)std::max(m, 1)));
+    CK(launch_subdiag(S, lds, m, c->sub.as<double>(), st));
+    launches += (m > 1);
+    if (m > 1) CK(cudaMemcpyAsync(sub.data(), c->sub.p, sizeof(double) * (m - 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   std::vector<int> bs, bz;
   int nb = blocks_host(m, sub.data(), bs, bz);
   if (nb < 0) return nb;
@@ -293,6 +318,25 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     int init[16] = {0x7fffffff, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(P.status, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
+  // block range of every tile (for the per-panel pair kernel of the host-staged path)
+  std::vector<int> tile_blk((size_t)M + 1, nb);
+  for (int p = nb - 1; p >= 0; --p) tile_blk[row_tile[bs[p]]] = p;
+  for (int I = M - 1; I >= 0; --I) tile_blk[I] = std::min(tile_blk[I], tile_blk[I + 1]);
+  if (hs) {
+    if ((int)hs->ev->size() < M) {
+      for (cudaEvent_t e : *hs->ev) cudaEventDestroy(e);
+      hs->ev->assign((size_t)M, nullptr);
+      for (auto& e : *hs->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (int I = M - 1; I >= 0; --I) {
+      const int rows = std::min(ts[I + 1] + 1, m), ncol = ts[I + 1] - ts[I];
+      CK(cudaMemcpy2DAsync((void*)(S + (size_t)ts[I] * lds), (size_t)lds * 8, hs->Sh + (size_t)ts[I] * hs->ldsh,
+                           (size_t)hs->ldsh * 8, (size_t)rows * 8, ncol, cudaMemcpyHostToDevice, hs->copy));
+      CK(cudaMemcpy2DAsync((void*)(T + (size_t)ts[I] * ldt), (size_t)ldt * 8, hs->Th + (size_t)ts[I] * hs->ldth,
+                           (size_t)hs->ldth * 8, (size_t)rows * 8, ncol, cudaMemcpyHostToDevice, hs->copy));
+      CK(cudaEventRecord((*hs->ev)[I], hs->copy));
+    }
+  }
   // TMA needs 16-byte aligned bases and even leading dimensions; otherwise repack
   const double* Su = S;
   const double* Tu = T;
@@ -311,10 +355,12 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   if ((lds & 1) || !aligned16(S)) { int r = repack(c->Sc, S, lds, 0, Su, ldsu); if (r) return r; }
   if ((ldt & 1) || !aligned16(T)) { int r = repack(c->Tc, T, ldt, 0, Tu, ldtu); if (r) return r; }
   // ---- a2 pairs, a3 norms (second host sync: status + pre-scale test) ----
-  for (int pass = 0; pass < 2; ++pass) {
+  // (host-staged path: per panel inside the wavefront, checked after it)
+  if (hs) CK(cudaMemsetAsync(P.cS, 0, sizeof(double) * 4 * M, st));
+  for (int pass = 0; pass < 2 && !hs; ++pass) {
     CK(cudaMemsetAsync(P.cS, 0, sizeof(double) * 4 * M, st));
-    CK(launch_pairs(Su, ldsu, Tu, ldtu, nb, P, st));
-    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st));
+    CK(launch_pairs(Su, ldsu, Tu, ldtu, 0, nb, P, st));
+    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st, 0, M));
     launches += 2 + (M > 1);
     std::vector<double> nrm(4 * (size_t)M);
     int stat[16];
@@ -360,7 +406,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     int init[16] = {0x7fffffff, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(P.status, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
-  if (n_sel == 0) {
+  if (n_sel == 0 && !hs) {
     c->info = info;
     return 0;
   }
@@ -382,6 +428,13 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   }
   int n_upd = 0;
   for (int I = M - 1; I >= 0; --I) {
+    if (hs) {
+      // panel I has arrived: its eigenvalue pairs and column-panel norms
+      CK(cudaStreamWaitEvent(st, (*hs->ev)[I], 0));
+      CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, st));
+      CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st, I, 1));
+      launches += 2;
+    }
     if (tile_item[I] >= n_items) continue;
     DiagParams dp;
     dp.I = I;
@@ -448,7 +501,25 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   CK(cudaEventRecord(c->e3, st));
   int stat[16];
   CK(cudaMemcpyAsync(stat, P.status, sizeof(stat), cudaMemcpyDeviceToHost, st));
+  std::vector<double> nrm(hs ? 4 * (size_t)M : 0);
+  if (hs) CK(cudaMemcpyAsync(nrm.data(), P.cS, sizeof(double) * 4 * M, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (hs) {
+    // deferred checks of the host-staged path: pair status, then the pre-scale test (R6);
+    // a pencil that needs the pre-scale is solved again on the (now complete) device copy
+    if (stat[0] != 0x7fffffff) {
+      int p = stat[0] >> 2, kind = stat[0] & 3;
+      return kind == 1 ? ZZ_ERR_NONFINITE : bs[p] + 1;
+    }
+    info.n_indefinite = stat[2];
+    double bS = 0, bT = 0, mdS = 0, mdT = 0;
+    for (int I = 0; I < M; ++I) {
+      bS += nrm[I]; bT += nrm[M + I];
+      mdS = std::max(mdS, nrm[2 * M + I]); mdT = std::max(mdT, nrm[3 * M + I]);
+    }
+    if (bS + mdS > 0x1p1020 || bT + mdT > 0x1p1020)
+      return tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, cse, nullptr);
+  }
   info.n_scaled = stat[4];
   info.min_exp = stat[5];
   info.update_launches = n_upd;
@@ -549,10 +620,15 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
   CK(c->hT.ensure(sizeof(double) * (size_t)ld * m));
   CK(c->hX.ensure(sizeof(double) * (size_t)ld * std::max(n_sel, 1)));
   CK(c->hE.ensure(sizeof(int) * (size_t)std::max(n_sel, 1)));
-  CK(cudaMemcpy2DAsync(c->hS.p, ld * 8, S, (size_t)lds * 8, (size_t)m * 8, m, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpy2DAsync(c->hT.p, ld * 8, T, (size_t)ldt * 8, (size_t)m * 8, m, cudaMemcpyHostToDevice, st));
+  if (!c->copy) CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  // the copy stream starts after everything already queued on the context's stream
+  if (!c->e_copy) CK(cudaEventCreateWithFlags(&c->e_copy, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->e_copy, st));
+  CK(cudaStreamWaitEvent(c->copy, c->e_copy, 0));
+  HostStage hs;
+  hs.Sh = S; hs.ldsh = lds; hs.Th = T; hs.ldth = ldt; hs.copy = c->copy; hs.ev = &c->ev_copy;
   int r = tgevc_device(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
-                       c->hE.as<int>());
+                       c->hE.as<int>(), &hs);
   if (r) return r;
   if (n_sel > 0) {
     CK(cudaMemcpy2DAsync(X, (size_t)ldx * 8, c->hX.p, ld * 8, (size_t)m * 8, n_sel, cudaMemcpyDeviceToHost, st));

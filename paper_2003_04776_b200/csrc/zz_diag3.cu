@@ -331,9 +331,9 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         // the whole segment by 2^(k+eu): pending rows in registers, the block's rows in the slab
         const int kk = k + eu;
         s.scale(kk);
-        __syncwarp();
+        // slot r of the slab is always written by lane r & 3 of its column (here and in the
+        // update below), so no warp barrier is needed in this column-divergent branch
         for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], kk);
-        __syncwarp();
         ex += kk;
         if (eu < 0) {
           xnb = scale2k(xnb, eu);
@@ -354,17 +354,15 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
           const double ur = beta * xo;
           const double wr = PAIR ? (comp ? (a * x.im + b * x.re) : (a * x.re - b * x.im)) : a * x.re;
           const double2* col = sm.ST + poff3(sidx ? j : j - 1) + (g8 - 1);
-          for (int r = q0 + t; r < qs; r += 4) {
+          for (int r = q0 + ((t - q0) & 3); r < qs; r += 4) {
             const double2 v = col[r];
             wslab[r * 8 + team] = fma(v.y, wr, fma(-v.x, ur, wslab[r * 8 + team]));
           }
         }
       }
-      // the solution into the slab (own component)
-      if (t == 0) {
-        wslab[q * 8 + team] = PAIR ? (comp ? xb.im : xb.re) : xb.re;
-        if (two) wslab[(q - 1) * 8 + team] = PAIR ? (comp ? xt.im : xt.re) : xt.re;
-      }
+      // the solution into the slab (own component; slot r by lane r & 3)
+      if (t == (q & 3)) wslab[q * 8 + team] = PAIR ? (comp ? xb.im : xb.re) : xb.re;
+      if (two && t == ((q - 1) & 3)) wslab[(q - 1) * 8 + team] = PAIR ? (comp ? xt.im : xt.re) : xt.re;
       __syncwarp();
       j = qs - 1 + (g8 - 1);
     }

@@ -143,7 +143,7 @@ size_t diag2_smem_bytes(int nt);
 cudaError_t launch_diag3(const Diag2Params& p, cudaStream_t st);
 size_t diag3_smem_bytes(int nt);
 cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, cudaStream_t st);
-cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int nblk,
+cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int p0, int nblk,
                          const DevPlan& P, cudaStream_t st);
 cudaError_t launch_maxabs(const double* S, long long lds, const double* T, long long ldt, int m,
                           unsigned long long* out, cudaStream_t st);
@@ -152,7 +152,7 @@ cudaError_t launch_rowsum_max(const double* A, long long lda, int m, unsigned lo
 cudaError_t launch_scale_copy(const double* A, long long lda, int m, int k, double* B, long long ldb,
                               cudaStream_t st);
 cudaError_t launch_panel_norms(const double* S, long long lds, const double* T, long long ldt, int M,
-                               const int* tile_start_host, const DevPlan& P, cudaStream_t st);
+                               const int* tile_start_host, const DevPlan& P, cudaStream_t st, int J0, int nJ);
 cudaError_t launch_diag(const DiagParams& p, cudaStream_t st);
 cudaError_t launch_normalize(int m, int n_sel, int M, double* X, long long ldx, int* col_scale_exp,
                              const DevPlan& P, int* exp_tmp, double* rec_tmp, cudaStream_t st);

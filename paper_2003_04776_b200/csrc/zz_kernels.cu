@@ -68,9 +68,10 @@ __device__ int pair_2x2(double s11, double s21, double s12, double s22, double t
 }
 
 __global__ void k_pairs(const double* __restrict__ S, long long lds, const double* __restrict__ T,
-                        long long ldt, int nblk, DevPlan P) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nblk) return;
+                        long long ldt, int p0, int nblk, DevPlan P) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nblk) return;
+  const int p = p0 + idx;
   int j = P.blk_start[p], sz = P.blk_size[p];
   double a, b, beta;
   int kind = kReal, err = 0;
@@ -107,10 +108,10 @@ __global__ void k_pairs(const double* __restrict__ S, long long lds, const doubl
     P.col_a[c + 1] = a; P.col_b[c + 1] = b; P.col_beta[c + 1] = beta; P.col_kind[c + 1] = kPairSecond;
   }
 }
-cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int nblk,
+cudaError_t launch_pairs(const double* S, long long lds, const double* T, long long ldt, int p0, int nblk,
                          const DevPlan& P, cudaStream_t st) {
   if (nblk <= 0) return cudaSuccess;
-  k_pairs<<<(nblk + 127) / 128, 128, 0, st>>>(S, lds, T, ldt, nblk, P);
+  k_pairs<<<(nblk + 127) / 128, 128, 0, st>>>(S, lds, T, ldt, p0, nblk, P);
   return cudaGetLastError();
 }
 
@@ -168,9 +169,9 @@ cudaError_t launch_scale_copy(const double* A, long long lda, int m, int k, doub
 // ------------------------------------------------------------------------------------
 __global__ void k_panel_norms(const double* __restrict__ S, long long lds,
                               const double* __restrict__ T, long long ldt,
-                              const int* __restrict__ tile_start, double* cS, double* cT,
+                              const int* __restrict__ tile_start, int J0, double* cS, double* cT,
                               double* dS, double* dT) {
-  int J = blockIdx.y + 1;
+  int J = J0 + blockIdx.y;
   int k0 = tile_start[J], k1 = tile_start[J + 1];
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (blockIdx.x * blockDim.x >= k1) return;
@@ -226,17 +227,23 @@ __global__ void k_diag0_norms(const double* __restrict__ S, long long lds,
   }
 }
 cudaError_t launch_panel_norms(const double* S, long long lds, const double* T, long long ldt, int M,
-                               const int* tile_start_host, const DevPlan& P, cudaStream_t st) {
-  // cS, cT, dS, dT are 4 consecutive arrays of M doubles (zeroed by the caller)
+                               const int* tile_start_host, const DevPlan& P, cudaStream_t st, int J0, int nJ) {
+  // cS, cT, dS, dT are 4 consecutive arrays of M doubles (zeroed by the caller); panels
+  // J0 .. J0+nJ-1 (J = 0 is the first tile's diagonal part only)
   double* dS = P.cS + 2 * (long long)M;
   double* dT = P.cS + 3 * (long long)M;
-  int m = tile_start_host[M];
-  if (M > 1) {
-    dim3 grid((m + 255) / 256, M - 1);
-    k_panel_norms<<<grid, 256, 0, st>>>(S, lds, T, ldt, P.tile_start, P.cS, P.cT, dS, dT);
+  if (nJ <= 0) return cudaSuccess;
+  if (J0 == 0) {
+    int k1 = tile_start_host[1];
+    k_diag0_norms<<<(k1 + 255) / 256, 256, 0, st>>>(S, lds, T, ldt, P.tile_start, dS, dT);
+    J0 = 1;
+    nJ -= 1;
   }
-  int k1 = tile_start_host[1];
-  k_diag0_norms<<<(k1 + 255) / 256, 256, 0, st>>>(S, lds, T, ldt, P.tile_start, dS, dT);
+  if (nJ > 0) {
+    int rows = tile_start_host[J0 + nJ];
+    dim3 grid((rows + 255) / 256, nJ);
+    k_panel_norms<<<grid, 256, 0, st>>>(S, lds, T, ldt, P.tile_start, J0, P.cS, P.cT, dS, dT);
+  }
   return cudaGetLastError();
 }
 

@@ -351,3 +351,46 @@ def test_C4_full_size_sampled(zz):
     assert ali.max() <= TOL and raw.max() <= TOL, (raw.max(), ali.max())
     assert (ed.cpu().numpy() <= 0).all()
     assert _gpu_residual(Sg, Tg, Xd, ref["pairs"], S, cols=cols) <= 10 * m * U
+
+
+def _host_solve(zz, S, T, mb, select=None, ldx=None):
+    """zz_tgevc_host: host S, T, X (the end-to-end path bench.py times)"""
+    zz.set_tile(mb)
+    m = S.shape[0]
+    n = oracle.count_columns(S, select)
+    X = np.full((ldx or m, max(n, 1)), np.nan, order="F")[:m, :n]
+    e = np.zeros(max(n, 1), np.int32)[:n]
+    zz.tgevc_host(S, T, select=select, X=X, col_scale_exp=e)
+    return X, e, zz.last_info()
+
+
+@pytest.mark.parametrize("name,seed,mb", [("C1", 0, 32), ("C1", 4, 64), ("C2", 1, 128), ("C2", 2, 64)])
+def test_host_path_bitwise_equal_to_device_path(zz, name, seed, mb):
+    """The host-staged path (panels copied in consumption order, overlapped with the solve)
+    computes exactly the device path's arithmetic."""
+    S, T, _ = gen.config(name, seed=seed)
+    X0, e0, i0 = solve(zz, S, T, mb=mb)
+    X1, e1, i1 = _host_solve(zz, S, T, mb)
+    assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
+    assert i1["n_tiles"] == i0["n_tiles"]
+    check_against_oracle(S, T, X1, e1)
+
+
+def test_host_path_select_ld_errors_and_prescale(zz):
+    S, T, _ = gen.config("C2", seed=0, m=700, n2=105)
+    rng = np.random.default_rng(3)
+    sel = (rng.random(700) < 0.2).astype(np.int32)
+    X0, e0, _ = solve(zz, S, T, mb=64, select=sel)
+    X1, e1, _ = _host_solve(zz, S, T, 64, select=sel, ldx=703)
+    assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
+    # status +j detected after the overlapped solve; X is not written
+    Sb = np.array([[0.5, 0.1, 0.2, 0.1], [0.0, 1.0, 0.3, 0.2], [0.0, 1.0, 1.0, 0.3], [0, 0, 0, 2.0]], order="F")
+    with pytest.raises(zz.ZZError) as ei:
+        _host_solve(zz, Sb, np.eye(4, order="F"), 32)
+    assert ei.value.status == 2
+    # entries near Omega/4: the deferred pre-scale test re-solves on the device copy (R6)
+    S2, T2, _ = gen.config("C1", seed=6)
+    Xr, er, _ = solve(zz, S2, T2, mb=32)
+    X2, e2, info = _host_solve(zz, np.asfortranarray(np.ldexp(S2, 1021)), np.asfortranarray(np.ldexp(T2, 1021)), 32)
+    assert info["prescaled"] == 1
+    assert np.array_equal(X2, Xr)
