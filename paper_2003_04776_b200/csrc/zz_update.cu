@@ -315,15 +315,16 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
       sy[ni] = 0;
       ld1p_i(sy[ni], p.sY + (ld ? c : 0), ld);
       const double* xc = p.X + (long long)(ld ? c : 0) * p.ldx;
+      // one 16-byte load per row pair (X is 16-byte aligned with an even ldx on this path),
+      // all issued before any is consumed
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi) {
         const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
-        const bool both = ld && (i0 + 1 < p.rows);
         acc[ni][mi][0] = 0.0;
         acc[ni][mi][1] = 0.0;
-        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, both && p.vec);
-        ld1p(acc[ni][mi][0], xc + i0, ld && i0 < p.rows && !(both && p.vec));
-        ld1p(acc[ni][mi][1], xc + i0 + 1, both && !p.vec);
+        // a pair straddling the last row is loaded whole (row p.rows exists: p.rows < m <=
+        // ldx); that accumulator row is never stored nor counted in the column maximum
+        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, ld && (i0 < p.rows));
       }
     }
 #pragma unroll
@@ -378,9 +379,8 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
         const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
         const bool both = cvalid && (i0 + 1 < p.rows);
-        st2p(xc + i0, v0, v1, both && p.vec);
-        st1p(xc + i0, v0, cvalid && i0 < p.rows && !(both && p.vec));
-        st1p(xc + i0 + 1, v1, both && !p.vec);
+        st2p(xc + i0, v0, v1, both);
+        st1p(xc + i0, v0, cvalid && i0 + 1 == p.rows);
         if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
         if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
       }
@@ -450,9 +450,10 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
-  if (ver == 2) return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
-  if (ver == 3) return launch_t<2, 4>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
-  if (ver == 4) return launch_t<4, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  // the template kernels move C in 16-byte pairs: X 16-byte aligned with an even ldx
+  if (ver == 2 && p.vec) return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 3 && p.vec) return launch_t<2, 4>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 4 && p.vec) return launch_t<4, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   dim3 g1(n_ntiles, n_mtiles);
   k_update_v1<<<g1, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
   return cudaGetLastError();
