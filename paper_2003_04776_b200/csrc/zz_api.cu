@@ -246,8 +246,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     rbeg[I] = (int)(std::lower_bound(real_tile.begin(), real_tile.end(), I) - real_tile.begin());
     pbeg[I] = (int)(std::lower_bound(pair_tile.begin(), pair_tile.end(), I) - pair_tile.begin());
   }
-  // diagonal-solve kernel: 3 = 8 columns per warp with DMMA in-tile updates (default),
-  // 2 = thread per eigenvector with sub-tile warps, 1 = warp per eigenvector (any tile)
+  // diagonal-solve kernel: 3 = 8 columns per warp with DMMA in-tile updates (default, tiles
+  // of <= 128 rows), 1 = warp per eigenvector (any tile; used above 128 rows)
   static const int diag_kind = getenv("ZZ_DIAG") ? atoi(getenv("ZZ_DIAG")) : 3;
   // ---- workspace ----
   const int n = std::max(n_sel, 1);
@@ -450,7 +450,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     dp.X = X; dp.ldx = ldx;
     dp.P = P;
     dp.nY_in = I & 1;
-    if (dp.nt <= kDiag2MaxNT && diag_kind >= 2) {
+    if (dp.nt <= kDiag2MaxNT && diag_kind != 1) {
       Diag2Params d2;
       d2.I = I; d2.t0 = dp.t0; d2.nt = dp.nt;
       d2.n_real = (int)real_list.size() - rbeg[I];
@@ -465,7 +465,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.X = X; d2.ldx = ldx;
       d2.P = P;
       d2.nY_in = dp.nY_in;
-      CK(diag_kind == 2 ? launch_diag2(d2, st) : launch_diag3(d2, st));
+      CK(launch_diag3(d2, st));
     } else {
       CK(launch_diag(dp, st));
     }

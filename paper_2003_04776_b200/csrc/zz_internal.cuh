@@ -118,7 +118,7 @@ struct UpdParams {
   int vec;           // 16-byte aligned X access possible
 };
 
-// Thread-per-eigenvector diagonal solve (zz_diag.cu): tiles of at most kDiag2MaxNT rows.
+// Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.
 constexpr int kDiag2MaxNT = 128;
 
 struct Diag2Params {
@@ -138,8 +138,6 @@ struct Diag2Params {
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)
-cudaError_t launch_diag2(const Diag2Params& p, cudaStream_t st);
-size_t diag2_smem_bytes(int nt);
 cudaError_t launch_diag3(const Diag2Params& p, cudaStream_t st);
 size_t diag3_smem_bytes(int nt);
 cudaError_t launch_subdiag(const double* S, long long lds, int m, double* sub, cudaStream_t st);
