@@ -58,13 +58,14 @@ struct Sm3 {
   double2* tau;    // per block b: max over rows i < s_b of the sums over the block's rows
   int* bs;         // block b = rows [bs[b], bs[b+1]); bs[b] = 8b - (row 8b is a 2x2 bottom)
   double* slab;    // per warp: the current block's rows, [9 slots][8 columns]
+  double* pslab;   // per warp: prepared pivots of the block's 1x1 rows, [9][8][8]
   signed char* fl; // row flags
 };
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ __forceinline__ size_t smem3(int nt) {
   return a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3)) + a16(sizeof(double2) * (size_t)nt) +
-         a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(sizeof(double) * 16 * 72) + a16((size_t)nt);
+         a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(sizeof(double) * 16 * 72) + a16(sizeof(double) * 16 * 576) + a16((size_t)nt);
 }
 __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt) {
   Sm3 s;
@@ -74,6 +75,7 @@ __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt) {
   s.tau = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * 17);
   s.bs = reinterpret_cast<int*>(base + o); o += a16(sizeof(int) * 18);
   s.slab = reinterpret_cast<double*>(base + o); o += a16(sizeof(double) * 16 * 72);
+  s.pslab = reinterpret_cast<double*>(base + o); o += a16(sizeof(double) * 16 * 576);
   s.fl = reinterpret_cast<signed char*>(base + o);
   return s;
 }
@@ -210,7 +212,8 @@ __device__ __forceinline__ double pending_max(const Seg<G>& s, int rot, int t, i
 // One task: 8 real columns (PAIR = false) or 4 complex pairs (PAIR = true) of tile I.
 // ------------------------------------------------------------------------------------
 template <int G, bool PAIR>
-__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, double* wslab) {
+__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, double* wslab,
+                           double* pslab) {
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
@@ -266,8 +269,38 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     wslab[(1 + 2 * t) * 8 + team] = s.y[CUR][0];
     wslab[(2 + 2 * t) * 8 + team] = s.y[CUR][1];
     if (t == 3) wslab[team] = s.y[PRV][1];
-    __syncwarp();
     const int q0 = s0 - (g8 - 1);
+    // pivots of the block's 1x1 rows, off the dependency chain: lane t prepares slots t,
+    // t+4, t+8 of its column -- the perturbed pivot d (R8), its reciprocal (real) or Smith's
+    // ratio and denominator (pair), and the ProtectDivision threshold (|w| <= thr: no scaling)
+    for (int q = t; q < 9; q += 4) {
+      const int j = g8 - 1 + q;
+      if (q < q0 || j >= e0 || sm.fl[j] != kRow1x1) continue;
+      const double2 dd = sm.ST[poff3(j) + j];
+      cpx d = mkc(__fma_rn(-a, dd.y, __dmul_rn(beta, dd.x)), __dmul_rn(-b, dd.y));
+      const double smin =
+          dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, fabs(dd.x)), __dmul_rn(ab, fabs(dd.y)))), kSmlnum);
+      if (n1(d) < smin) d = mkc(smin, 0.0);
+      double* pd = pslab + (q * 8 + team) * 8;
+      pd[0] = d.re;
+      pd[1] = d.im;
+      if (!PAIR) {
+        const double td = fabs(d.re);
+        pd[2] = __drcp_rn(d.re);
+        pd[3] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
+      } else {
+        const double td = __dmul_rn(0.5, dmind(1.0, nmax(d)));
+        const bool re_dom = fabs(d.re) >= fabs(d.im);
+        const double sr = re_dom ? __ddiv_rn(d.im, d.re) : __ddiv_rn(d.re, d.im);
+        const double den = re_dom ? __dadd_rn(d.re, __dmul_rn(d.im, sr)) : __dadd_rn(d.im, __dmul_rn(d.re, sr));
+        pd[2] = sr;
+        pd[3] = den;
+        pd[4] = __drcp_rn(den);
+        pd[5] = re_dom ? 1.0 : 0.0;
+        pd[6] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
+      }
+    }
+    __syncwarp();
     int j = e0 - 1;
     while (j >= s0) {
       const int q = j - (g8 - 1);
@@ -300,8 +333,31 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
           xt = wt;
           xb = wb;
         } else {
-          const double2 d = sm.ST[poff3(j) + j];
-          xb = solve1x1<PAIR>(wb, d.x, d.y, a, b, beta, ab, k);
+          // (beta S_jj - alpha T_jj) x = w with the prepared pivot: q = w r corrected once by
+          // the residual (the quotient of __ddiv_rn); scaling only past the threshold
+          const double* pd = pslab + (q * 8 + team) * 8;
+          const cpx d = mkc(pd[0], pd[1]);
+          if (!PAIR) {
+            const double r = pd[2];
+            if (fabs(wb.re) <= pd[3]) {
+              const double x0 = wb.re * r;
+              xb = mkc(fma(r, fma(-d.re, x0, wb.re), x0), 0.0);
+            } else {
+              xb = pdiv3<false>(wb, d, k);
+            }
+          } else {
+            if (nmax(wb) <= pd[6]) {
+              const double sr = pd[2], den = pd[3], rd = pd[4];
+              const double n1v = (pd[5] != 0.0) ? __dadd_rn(wb.re, __dmul_rn(wb.im, sr))
+                                                : __dadd_rn(__dmul_rn(wb.re, sr), wb.im);
+              const double n2v = (pd[5] != 0.0) ? __dsub_rn(wb.im, __dmul_rn(wb.re, sr))
+                                                : __dsub_rn(__dmul_rn(wb.im, sr), wb.re);
+              const double y1 = n1v * rd, y2 = n2v * rd;
+              xb = mkc(fma(rd, fma(-den, y1, n1v), y1), fma(rd, fma(-den, y2, n2v), y2));
+            } else {
+              xb = pdiv3<true>(wb, d, k);
+            }
+          }
           if (!PAIR && tip && tipr == j) { xb = mkc(1.0, 0.0); k = 0; }
           xt = xb;
         }
@@ -594,9 +650,10 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   // ---- tasks: 4 complex pairs or 8 real columns per warp ----
   const int npt = (p.n_pair + 3) / 4, nrt = (p.n_real + 7) / 8;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two
+  // (measured: contiguous per-CTA task ranges were slower, pair tasks being heavier)
   for (int task = warp * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * kW3) {
-    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, sm.slab + warp * 72);
-    else solve_task<G, false>(p, sm, nblk, task - npt, lane, sm.slab + warp * 72);
+    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, sm.slab + warp * 72, sm.pslab + warp * 576);
+    else solve_task<G, false>(p, sm, nblk, task - npt, lane, sm.slab + warp * 72, sm.pslab + warp * 576);
   }
 }
 
