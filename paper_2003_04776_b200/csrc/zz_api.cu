@@ -58,7 +58,7 @@ struct Context {
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
-  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc;
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Apk;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> ev_copy;       // per-panel arrival events of zz_tgevc_host
@@ -68,7 +68,7 @@ struct Context {
   ~Context() {}
   void release() {
     Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
-                  &status, &tmp, &Sc, &Tc, &hS, &hT, &hX, &hE};
+                  &status, &tmp, &Sc, &Tc, &Apk, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
@@ -485,6 +485,13 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       up.sY = P.sY;
       up.nY_out = P.nY + (size_t)(1 - (I & 1)) * n;
       up.vec = vec;
+      up.Apk = nullptr;
+      if (update_packs()) {
+        CK(c->Apk.ensure(pack_bytes(ts[I], dp.nks)));
+        CK(launch_pack(Su, ldsu, Tu, ldtu, ts[I], ts[I], dp.nt, dp.nks, c->Apk.as<double>(), st));
+        up.Apk = c->Apk.as<double>();
+        launches++;
+      }
       int n_m = ceil_div(ts[I], kBM);
       int n_n = ceil_div(n_sel, kBN) - up.ntile0;
       if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));

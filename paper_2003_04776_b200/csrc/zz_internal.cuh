@@ -116,6 +116,7 @@ struct UpdParams {
   const int* sY;
   unsigned long long* nY_out;
   int vec;           // 16-byte aligned X access possible
+  const double* Apk; // S/T panel packed in fragment order (update_packs()), or null
 };
 
 // Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.
@@ -158,6 +159,12 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
                           int n_mtiles, int n_ntiles, cudaStream_t st);
 size_t diag_smem_bytes(int nt);
 int update_version();
+// The S/T panel of a step packed in the DMMA fragment order of the update kernel:
+// [m-tile][k-chunk][8-row group][k/4][row in group][k%4], one 16 KB block per stage.
+bool update_packs();
+size_t pack_bytes(int rows, int nks);
+cudaError_t launch_pack(const double* S, long long lds, const double* T, long long ldt, int rows, int t0, int nt,
+                        int nks, double* Apk, cudaStream_t st);
 int update_box_rows();   // rows per TMA box of the S/T tensor maps
 
 }  // namespace zz

@@ -228,6 +228,41 @@ __device__ __forceinline__ void ld1p_i(int& x, const int* p, bool pr) {
   asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.global.b32 %0, [%1];\n}" : "+r"(x) : "l"(p), "r"((int)pr));
 }
 
+// S/T panel of step I in fragment order: block (mt, kc) holds rows mt*128 .. +127 and the 16
+// columns of chunk kc (S for kc < nks, T after), element (row 8g + c, column 4s + r) at
+// ((g * 4 + s) * 8 + c) * 4 + r -- lane (c, r) of a DMMA B fragment reads consecutive doubles.
+// Rows >= rows and columns >= nt are zero.  One CTA per block, staged through shared memory
+// (coalesced column-major reads, contiguous writes).
+__global__ void __launch_bounds__(256) k_pack(const double* __restrict__ S, long long lds, const double* __restrict__ T,
+                                              long long ldt, int rows, int t0, int nt, int nks, double* __restrict__ Apk) {
+  __shared__ double tile[16][129];
+  const int mt = blockIdx.x, kc = blockIdx.y;
+  const double* A = (kc < nks) ? S : T;
+  const long long lda = (kc < nks) ? lds : ldt;
+  const int c0 = (kc % nks) * kBK;
+  for (int idx = threadIdx.x; idx < 16 * 128; idx += 256) {
+    const int col = idx >> 7, r = idx & 127;
+    const int gr = mt * kBM + r, gc = c0 + col;
+    tile[col][r] = (gr < rows && gc < nt) ? A[(long long)(t0 + gc) * lda + gr] : 0.0;
+  }
+  __syncthreads();
+  double* out = Apk + ((long long)mt * (2 * nks) + kc) * (kBM * kBK);
+  for (int o = threadIdx.x; o < kBM * kBK; o += 256) {
+    const int rr = o & 3, c = (o >> 2) & 7, sidx = (o >> 5) & 3, g = o >> 7;
+    out[o] = tile[sidx * 4 + rr][g * 8 + c];
+  }
+}
+
+size_t pack_bytes(int rows, int nks) { return (size_t)((rows + kBM - 1) / kBM) * 2 * nks * kBM * kBK * 8; }
+
+cudaError_t launch_pack(const double* S, long long lds, const double* T, long long ldt, int rows, int t0, int nt,
+                        int nks, double* Apk, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  dim3 grid((rows + kBM - 1) / kBM, 2 * nks);
+  k_pack<<<grid, 256, 0, st>>>(S, lds, T, ldt, rows, t0, nt, nks, Apk);
+  return cudaGetLastError();
+}
+
 // Persistent: each CTA walks the (m-tile, n-tile) grid with stride gridDim.x; the producer
 // warp runs ahead into the next tile while the consumers finish the current epilogue.
 // WN column warps x 2 row warps consume a 128 x (32 WN) tile; WN = 4 is one 288-thread CTA
@@ -286,9 +321,15 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
           const int kcol = p.t0 + (kc % p.nks) * kBK;
           double* a = sA + s * (kBM * kBK);
-          // S/T chunk as [BM/BOX][BK][BOX] (BOX = 4: conflict-free fragment loads)
+          if (BOX == 0) {
+            // packed panel (k_pack): one 16 KB bulk copy per stage
+            bulk_load(a, p.Apk + ((long long)(m0 / kBM) * nkc + kc) * (kBM * kBK), kABytes, &full[s]);
+          } else {
+            // S/T chunk as [BM/BOX][BK][BOX] (BOX = 4: conflict-free fragment loads)
 #pragma unroll 4
-          for (int mo = 0; mo < kBM / BOX; ++mo) tma_load_2d(a + mo * (kBK * BOX), tm, m0 + mo * BOX, kcol, &full[s]);
+            for (int mo = 0; mo < kBM / BOX; ++mo)
+              tma_load_2d(a + mo * (kBK * BOX), tm, m0 + mo * BOX, kcol, &full[s]);
+          }
           for (int q = 0; q < nblk; ++q)
             bulk_load(sB + s * (C::BN * kBK) + q * (kBN * kBK), p.W + (long long)(nb64 + q) * wtile + (long long)kc * (kBN * kBK),
                       kBBytes, &full[s]);
@@ -351,7 +392,9 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wc + ni * 8 + cq) * 4 + rq];
 #pragma unroll
         for (int mi = 0; mi < 8; ++mi) {
-          if (BOX == 8) {
+          if (BOX == 0) {
+            fs[mi] = a[(((wm * 8 + mi) * 4 + ks) * 8 + cq) * 4 + rq];
+          } else if (BOX == 8) {
             fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
           } else {
             const int grp = wm * 16 + mi * 2 + (cq >> 2);
@@ -407,6 +450,7 @@ int update_version() {
   return ver;
 }
 int update_box_rows() { return update_version() == 3 ? 4 : 8; }
+bool update_packs() { return update_version() == 5; }
 
 template <int WN, int BOX>
 static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
@@ -454,6 +498,7 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
   if (ver == 2 && p.vec) return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   if (ver == 3 && p.vec) return launch_t<2, 4>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   if (ver == 4 && p.vec) return launch_t<4, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 5 && p.vec && p.Apk) return launch_t<2, 0>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   dim3 g1(n_ntiles, n_mtiles);
   k_update_v1<<<g1, kThreads, kSmemBytes, st>>>(*tmS, *tmT, p);
   return cudaGetLastError();
