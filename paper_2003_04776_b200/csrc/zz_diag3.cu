@@ -217,9 +217,13 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
-  const int item = PAIR ? task * 4 + (team >> 1) : task * 8 + team;
+  // cpt columns per task (8, 4 or 2: fewer when the step has few columns, so that more
+  // warps run; a column's arithmetic does not depend on the other columns of its warp)
+  const int cpt = p.cpt;
+  const int slot = PAIR ? (team >> 1) : team;
+  const int item = PAIR ? task * (cpt / 2) + slot : task * cpt + slot;
   const int n_items = PAIR ? p.n_pair : p.n_real;
-  const bool valid = item < n_items;
+  const bool valid = item < n_items && slot < (PAIR ? cpt / 2 : cpt);
   const int c0 = valid ? (PAIR ? p.pair_items[item] : p.real_items[item]) : -1;
   const int c = c0 + comp;                       // this lane's output column
   double a = 0.0, b = 0.0, beta = 0.0;
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   }
   __syncthreads();
   // ---- tasks: 4 complex pairs or 8 real columns per warp ----
-  const int npt = (p.n_pair + 3) / 4, nrt = (p.n_real + 7) / 8;
+  const int npt = (p.n_pair + p.cpt / 2 - 1) / (p.cpt / 2), nrt = (p.n_real + p.cpt - 1) / p.cpt;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two
   // (measured: contiguous per-CTA task ranges were slower, pair tasks being heavier)
   for (int task = warp * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * kW3) {
@@ -663,15 +667,21 @@ int g_sms3 = 0;
 
 size_t diag3_smem_bytes(int nt) { return smem3(nt); }
 
-cudaError_t launch_diag3(const Diag2Params& p, cudaStream_t st) {
-  const int tasks = (p.n_pair + 3) / 4 + (p.n_real + 7) / 8;
-  if (tasks == 0) return cudaSuccess;
-  if (p.nt > kDiag2MaxNT) return cudaErrorInvalidValue;
+cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
+  Diag2Params p = pin;
   if (!g_sms3) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms3, cudaDevAttrMultiProcessorCount, dev);
   }
+  // columns per task: 8, halved while the step has fewer tasks than warp slots
+  const int slots = g_sms3 * (p.nt <= 64 ? W3<8>::n : W3<16>::n);
+  p.cpt = 8;
+  auto ntask = [&](int cpt) { return (p.n_pair + cpt / 2 - 1) / (cpt / 2) + (p.n_real + cpt - 1) / cpt; };
+  while (p.cpt > 2 && ntask(p.cpt) < slots) p.cpt /= 2;
+  const int tasks = ntask(p.cpt);
+  if (tasks == 0) return cudaSuccess;
+  if (p.nt > kDiag2MaxNT) return cudaErrorInvalidValue;
   const size_t smem = smem3(p.nt);
   cudaError_t e;
   if (p.nt <= 64) {

@@ -136,6 +136,7 @@ struct Diag2Params {
   double* X; long long ldx;
   DevPlan P;
   int nY_in;
+  int cpt;                 // columns per warp task (set by launch_diag3)
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)
