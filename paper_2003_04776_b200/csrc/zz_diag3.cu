@@ -674,12 +674,10 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms3, cudaDevAttrMultiProcessorCount, dev);
   }
-  // columns per task: 8, halved while the step has fewer tasks than warp slots
-  const int slots = g_sms3 * (p.nt <= 64 ? W3<8>::n : W3<16>::n);
+  // 8 columns per task (measured: 4 or 2 columns per task on steps with few columns were
+  // slower -- more tasks, more instruction-cache pressure, no shorter chain per task)
   p.cpt = 8;
-  auto ntask = [&](int cpt) { return (p.n_pair + cpt / 2 - 1) / (cpt / 2) + (p.n_real + cpt - 1) / cpt; };
-  while (p.cpt > 2 && ntask(p.cpt) < slots) p.cpt /= 2;
-  const int tasks = ntask(p.cpt);
+  const int tasks = (p.n_pair + 3) / 4 + (p.n_real + 7) / 8;
   if (tasks == 0) return cudaSuccess;
   if (p.nt > kDiag2MaxNT) return cudaErrorInvalidValue;
   const size_t smem = smem3(p.nt);
