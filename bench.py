@@ -301,6 +301,7 @@ def main():
     value = F / t * 1e-12
     zz.set_timing(False)
     info = zz.last_info()
+    info_upd_launches = info["update_launches"]
 
     res = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -313,9 +314,10 @@ def main():
                       "phase_ms_last_step": {k: info[k] for k in ("ms_setup", "ms_steps", "ms_normalize")}},
            "gpu_launches": launches}
     # roofline of the dominant kernel (the robust update, k_update)
-    upd_avg = upd_ms / max(1, args.steps * max(1, len(per_launch)))
+    n_upd_launch = max(1, info_upd_launches)
+    upd_avg = upd_ms / max(1, args.steps * n_upd_launch)
     if upd_ms > 0:
-        ach = (F_upd / len(per_launch)) / (upd_avg * 1e-3) * 1e-12
+        ach = (F_upd / n_upd_launch) / (upd_avg * 1e-3) * 1e-12
         traffic, tnote = None, None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_update"]
@@ -326,7 +328,8 @@ def main():
         res["roofline"] = {"bound": "tensor", "kernel": "k_update (DMMA.8x8x4 FP64 contraction)",
                            "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
                            "traffic": traffic, "traffic_note": tnote, "peak_source": PEAK_SRC,
-                           "algorithmic_flops_per_launch": F_upd / len(per_launch),
+                           "algorithmic_flops_per_launch": F_upd / n_upd_launch,
+                           "update_launches_per_step": n_upd_launch,
                            "avg_launch_ms": upd_avg,
                            "share_of_step": upd_ms / args.steps / (t * 1e3)}
     res["clocks"] = clocks

@@ -60,6 +60,8 @@ typedef struct zz_info {
   int prescaled;      /* 1 if S or T was pre-scaled by a power of two (reading R6) */
   int update_launches;     /* robust-update kernel launches */
   int total_launches;      /* all kernel launches of the call */
+  int fused_pairs;         /* step pairs whose updates ran as one two-tile contraction */
+  int reserved;
   double ms_setup;         /* structure scan, pairs, norms */
   double ms_steps;         /* the wavefront (diagonal solves + updates) */
   double ms_normalize;     /* consistency and normalisation */
@@ -92,7 +94,10 @@ int zz_set_timing(int on);
  *                  eigenvalue j; a complex pair (j, j+1) is computed if either flag is
  *                  set.  Output columns are packed in block order.           [arg 6]
  *   X, ldx         DEVICE, m x n_sel column-major, ldx >= max(1,m); written
- *                  completely (including the zeros below each column's block)  [args 7,8]
+ *                  completely (including the zeros below each column's block).
+ *                  An odd ldx or a base not 16-byte aligned is solved in an internal
+ *                  aligned m x n_sel workspace and copied out: results are bitwise
+ *                  independent of ldx.                                          [args 7,8]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: e_c <= 0 such that the tip-normalised
  *                  eigenvector (x_r = 1) is 2^-e_c times the column before
  *                  normalisation (Definition 1).  Both columns of a

@@ -44,6 +44,7 @@ class Info(ctypes.Structure):
                 ("n_tiles", ctypes.c_int), ("n_scaled", ctypes.c_int), ("min_exp", ctypes.c_int),
                 ("n_indefinite", ctypes.c_int), ("prescaled", ctypes.c_int),
                 ("update_launches", ctypes.c_int), ("total_launches", ctypes.c_int),
+                ("fused_pairs", ctypes.c_int), ("reserved", ctypes.c_int),
                 ("ms_setup", ctypes.c_double), ("ms_steps", ctypes.c_double),
                 ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double)]
 

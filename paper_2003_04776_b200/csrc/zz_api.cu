@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -58,7 +59,7 @@ struct Context {
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
-  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Apk;
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, status, tmp, Sc, Tc, Apk, Xi;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> ev_copy;       // per-panel arrival events of zz_tgevc_host
@@ -67,8 +68,8 @@ struct Context {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   ~Context() {}
   void release() {
-    Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
-                  &status, &tmp, &Sc, &Tc, &Apk, &hS, &hT, &hX, &hE};
+    Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W, &W2,
+                  &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
@@ -85,10 +86,14 @@ struct Context {
 
 thread_local Context* g_ctx = nullptr;
 
-#define CK(x)                                   \
-  do {                                          \
-    cudaError_t _e = (x);                       \
-    if (_e != cudaSuccess) return map_err(_e);  \
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t _e = (x);                                                         \
+    if (_e != cudaSuccess) {                                                      \
+      if (getenv("ZZ_DEBUG_SYNC"))                                                \
+        fprintf(stderr, "zz: %s (line %d): %s\n", #x, __LINE__, cudaGetErrorString(_e)); \
+      return map_err(_e);                                                         \
+    }                                                                             \
   } while (0)
 
 int map_err(cudaError_t e) {
@@ -254,7 +259,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   const int nks_max = ceil_div(mb, kBK);
   const int n_ntiles_all = ceil_div(n, kBN);
   CK(c->colf.ensure(sizeof(double) * 3 * (size_t)n));
-  CK(c->coli.ensure(sizeof(int) * 7 * (size_t)n));
+  CK(c->coli.ensure(sizeof(int) * 9 * (size_t)n));
   CK(c->items.ensure(sizeof(int) * 2 * (size_t)std::max(n_items, 1)));
   CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
   CK(c->rows.ensure((sizeof(int) + 1) * (size_t)m + 16));
@@ -274,6 +279,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.col_tile = P.col_r + n;
   P.e_pend = P.col_tile + n;
   P.sY = P.e_pend + n;
+  P.e_prev = P.sY + n;
   P.item_col = c->items.as<int>();
   P.real_items = P.item_col + n_items;
   P.pair_items = P.real_items + real_list.size();
@@ -420,22 +426,55 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * 2 * n, st));
   CK(cudaEventRecord(c->e1, st));
   // ---- the wavefront (Algorithm 1 over tile rows, bottom-up) ----
+  // X with an odd leading dimension or a base that is not 16-byte aligned: solve into an
+  // aligned internal buffer and copy out once (below), so that every X runs the same kernels
+  // in the same order -- results are bitwise independent of ldx
+  double* Xout = nullptr;
+  long long ldxo = 0;
+  if (n_sel > 0 && (((ldx & 1) != 0) || !aligned16(X))) {
+    const long long ldi = (m + 1) & ~1LL;
+    CK(c->Xi.ensure(sizeof(double) * (size_t)ldi * n_sel));
+    Xout = X;
+    ldxo = ldx;
+    X = c->Xi.as<double>();
+    ldx = ldi;
+  }
   const int vec = ((ldx & 1) == 0) && aligned16(X);
   if (c->timing && (int)c->ev.size() < 2 * M) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     c->ev.assign(2 * (size_t)M, nullptr);
     for (auto& e : c->ev) cudaEventCreate(&e);
   }
-  int n_upd = 0;
-  for (int I = M - 1; I >= 0; --I) {
-    if (hs) {
-      // panel I has arrived: its eigenvalue pairs and column-panel norms
-      CK(cudaStreamWaitEvent(st, (*hs->ev)[I], 0));
-      CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, st));
-      CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st, I, 1));
-      launches += 2;
+  int n_upd = 0, n_fused = 0;
+  // Two-step fusion (ZZ_FUSE, default on with the k_diag3 / k_update_t path): for a pair of
+  // steps (I, J = I - 1) the rows of tile J get step I's update first (a thin update, one
+  // 128-row band), tile J is solved, and the rows above tile J get both steps' updates in one
+  // contraction with K = [tile J | tile I] (twice the K of a single step: half the C-tile
+  // traffic and prologue/epilogue per flop).
+  static const int fuse_env = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 1;
+  const bool can_fuse = fuse_env && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
+  CK(c->W2.ensure(c->W.cap));
+  int nyb = (M - 1) & 1;   // nY buffer holding the pending max for the next decision
+  static const bool dbg_sync = getenv("ZZ_DEBUG_SYNC") != nullptr;
+  auto dbg = [&](const char* what, int I) -> int {
+    if (!dbg_sync) return 0;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "zz: %s at step %d failed: %s\n", what, I, cudaGetErrorString(e));
+      return map_err(e);
     }
-    if (tile_item[I] >= n_items) continue;
+    return 0;
+  };
+  auto panel_ready = [&](int I) -> int {
+    if (!hs) return 0;
+    // panel I has arrived: its eigenvalue pairs and column-panel norms
+    CK(cudaStreamWaitEvent(st, (*hs->ev)[I], 0));
+    CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, st));
+    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st, I, 1));
+    launches += 2;
+    return 0;
+  };
+  auto diag = [&](int I, double* Wout, const Diag2Params* fuse_from) -> int {
     DiagParams dp;
     dp.I = I;
     dp.t0 = ts[I];
@@ -449,9 +488,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     dp.S = Su; dp.lds = ldsu; dp.T = Tu; dp.ldt = ldtu;
     dp.X = X; dp.ldx = ldx;
     dp.P = P;
-    dp.nY_in = I & 1;
+    dp.nY_in = nyb;
     if (dp.nt <= kDiag2MaxNT && diag_kind != 1) {
       Diag2Params d2;
+      memset(&d2, 0, sizeof(d2));
       d2.I = I; d2.t0 = dp.t0; d2.nt = dp.nt;
       d2.n_real = (int)real_list.size() - rbeg[I];
       d2.n_pair = (int)pair_list.size() - pbeg[I];
@@ -465,46 +505,104 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.X = X; d2.ldx = ldx;
       d2.P = P;
       d2.nY_in = dp.nY_in;
+      d2.Wout = Wout;
+      if (fuse_from) {
+        d2.fused = 1;
+        d2.Iprev = fuse_from->I;
+        d2.cs_prev = cs[fuse_from->I];
+        d2.zero_pend_end = cs[fuse_from->I + 1];
+        d2.Wprev = fuse_from->Wout;
+        d2.nks_prev = fuse_from->nks;
+      }
       CK(launch_diag3(d2, st));
     } else {
       CK(launch_diag(dp, st));
     }
     launches++;
+    return dbg(fuse_from ? "diag (fused)" : "diag", I);
+  };
+  auto update = [&](UpdParams up, int n_m) -> int {
+    const int n_n = ceil_div(n_sel, kBN) - up.ntile0;
+    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));
+    CK(launch_update(&tmS, &tmT, up, n_m, n_n, st));
+    if (int r = dbg(up.nksb ? "fused update" : (up.row_lo ? "thin update" : "update"), up.t0 / std::max(mb, 1))) return r;
+    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], st));
+    n_upd++;
+    launches++;
+    return 0;
+  };
+  auto base_up = [&](int I) {
+    UpdParams up;
+    memset(&up, 0, sizeof(up));
+    up.rows = ts[I];
+    up.max_row = (I > 0) ? ts[I - 1] : 0;
+    up.t0 = ts[I];
+    up.nks = ceil_div(ts[I + 1] - ts[I], kBK);
+    up.c_begin = cs[I];
+    up.first_end = cs[I + 1];
+    up.n_sel = n_sel;
+    up.ntile0 = cs[I] / kBN;
+    up.X = X; up.ldx = ldx;
+    up.W = P.W;
+    up.sY = P.sY;
+    up.nY_out = P.nY + (size_t)(1 - nyb) * n;
+    up.vec = vec;
+    return up;
+  };
+  int I = M - 1;
+  while (I >= 0) {
+    int r = panel_ready(I);
+    if (r) return r;
+    if (tile_item[I] >= n_items) { --I; continue; }
+    const int J = I - 1;
+    // pairs are fixed by the tile index alone ((M-1-I) even), not by which steps have active
+    // columns, so a column's operations do not depend on the selection (sharding, select)
+    if (can_fuse && J >= 1 && ((M - 1 - I) & 1) == 0) {
+      // ---- fused pair (I, J) ----
+      Diag2Params first;
+      first.I = I;
+      first.nks = ceil_div(ts[I + 1] - ts[I], kBK);
+      first.Wout = P.W;
+      if ((r = diag(I, P.W, nullptr))) return r;
+      UpdParams thin = base_up(I);          // rows of tile J only, no column maximum
+      thin.row_lo = ts[J];
+      thin.max_row = 0;
+      if ((r = update(thin, ceil_div(ts[I] - (ts[J] & ~1), kBM)))) return r;
+      if ((r = panel_ready(J))) return r;
+      if ((r = diag(J, c->W2.as<double>(), &first))) return r;
+      UpdParams fu = base_up(J);            // rows above tile J, K = [tile J | tile I]
+      fu.W = c->W2.as<double>();
+      fu.first_end = cs[I + 1];             // tips of I and J start from zero pending rows
+      fu.t0b = ts[I];
+      fu.nksb = first.nks;
+      fu.Wb = P.W;
+      if ((r = update(fu, ceil_div(ts[J], kBM)))) return r;
+      nyb = 1 - nyb;
+      ++n_fused;
+      I -= 2;
+      continue;
+    }
+    if ((r = diag(I, P.W, nullptr))) return r;
     if (I > 0) {
-      UpdParams up;
-      up.rows = ts[I];
-      up.max_row = ts[I - 1];
-      up.t0 = ts[I];
-      up.nks = dp.nks;
-      up.c_begin = cs[I];
-      up.first_end = cs[I + 1];
-      up.n_sel = n_sel;
-      up.ntile0 = cs[I] / kBN;
-      up.X = X; up.ldx = ldx;
-      up.W = P.W;
-      up.sY = P.sY;
-      up.nY_out = P.nY + (size_t)(1 - (I & 1)) * n;
-      up.vec = vec;
-      up.Apk = nullptr;
+      UpdParams up = base_up(I);
       if (update_packs()) {
-        CK(c->Apk.ensure(pack_bytes(ts[I], dp.nks)));
-        CK(launch_pack(Su, ldsu, Tu, ldtu, ts[I], ts[I], dp.nt, dp.nks, c->Apk.as<double>(), st));
+        CK(c->Apk.ensure(pack_bytes(ts[I], up.nks)));
+        CK(launch_pack(Su, ldsu, Tu, ldtu, ts[I], ts[I], ts[I + 1] - ts[I], up.nks, c->Apk.as<double>(), st));
         up.Apk = c->Apk.as<double>();
         launches++;
       }
-      int n_m = ceil_div(ts[I], kBM);
-      int n_n = ceil_div(n_sel, kBN) - up.ntile0;
-      if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));
-      CK(launch_update(&tmS, &tmT, up, n_m, n_n, st));
-      if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], st));
-      n_upd++;
-      launches++;
+      if ((r = update(up, ceil_div(ts[I], kBM)))) return r;
+      nyb = 1 - nyb;
     }
+    --I;
   }
   CK(cudaEventRecord(c->e2, st));
   // ---- a7 consistency and normalisation ----
   CK(launch_normalize(m, n_sel, M, X, ldx, cse, P, exp_tmp, rec_tmp, st));
   launches += 2;
+  if (Xout)
+    CK(cudaMemcpy2DAsync(Xout, sizeof(double) * ldxo, X, sizeof(double) * ldx, sizeof(double) * m, n_sel,
+                         cudaMemcpyDeviceToDevice, st));
   CK(cudaEventRecord(c->e3, st));
   int stat[16];
   CK(cudaMemcpyAsync(stat, P.status, sizeof(stat), cudaMemcpyDeviceToHost, st));
@@ -530,6 +628,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   info.n_scaled = stat[4];
   info.min_exp = stat[5];
   info.update_launches = n_upd;
+  info.fused_pairs = n_fused;
   info.total_launches = launches;
   float ms;
   cudaEventElapsedTime(&ms, c->e0, c->e1); info.ms_setup = ms;

@@ -518,7 +518,55 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       P.nrm_seg[so] = lm;
       P.nrmh_seg[so] = lh;
     }
-    if (p.do_update) {
+    if (p.do_update && p.fused) {
+      // second step J of a fused pair (I, J = I - 1): one update of the rows above tile J with
+      // both tiles (K = [tile J | tile I]).  Those rows are still at the exponent e_p they had
+      // before step I (step I only updated tile J's rows, the thin update); step I's W_I is at
+      // e1 = e_pend.  The decision bounds all three terms (Alg. 3 with the sum of the two
+      // panels' norms and the larger of the two aligned segment norms, R5):
+      //   2^(ef-e_p) y^ + 2^(ef-e1) tau_I |W_I| + tau_J 2^(ef-e_J) x^_J <= Omega.
+      const bool act_prev = c0 >= p.cs_prev;                  // active at step I
+      const int e1 = ep;
+      const int e_p = act_prev ? P.e_prev[c] : 0;              // written by step I only
+      const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
+      double nyv = 0.0;
+      if (c0 >= p.zero_pend_end) {                            // not a tip of I or J
+        nyv = __longlong_as_double((long long)nyi[c0]);
+        if (PAIR) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
+      }
+      double xI = 0.0;
+      int eI = 0;
+      if (act_prev) {
+        const long long sp = (long long)p.Iprev * p.n_sel + c;
+        xI = P.nrm_seg[sp];
+        eI = P.e_seg[sp];
+      }
+      const int g0 = min(e1, es);
+      const double yh = scale2k(nyv, g0 - e_p);
+      const double xh = dmaxd(act_prev ? scale2k(xI, g0 - eI) : 0.0, scale2k(lm, g0 - es));
+      // (a column not active at step I has no tile-I term: its decision is then exactly the
+      // single-step one)
+      double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
+      if (act_prev) tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Iprev]), __dmul_rn(ab, P.cT[p.Iprev])));
+      const int ef = g0 + protect_update(yh, tau, xh);
+      sx = ef - es;
+      if (t == 0) {
+        P.sY[c] = ef - e_p;
+        P.e_pend[c] = ef;
+        P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
+      }
+      // W_I of this column: rescaled to ef (rare), or zero for a tip of J (stale entries)
+      if (!act_prev || ef != e1) {
+        const long long tstr = (long long)(2 * p.nks_prev) * (kBN * kBK);
+        const long long hf = (long long)p.nks_prev * (kBN * kBK);
+        double* Wp = p.Wprev + (long long)(c / kBN) * tstr + (c % kBN) * 4;
+        for (int r = t; r < p.nks_prev * kBK; r += 4) {
+          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
+          Wp[off] = act_prev ? scale2k(Wp[off], ef - e1) : 0.0;
+          Wp[off + hf] = act_prev ? scale2k(Wp[off + hf], ef - e1) : 0.0;
+        }
+      }
+    } else if (p.do_update) {
       // Alg. 3 with Alg. 2, reading R5; pending max of the column
       // (pairs: of both columns)
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
@@ -531,6 +579,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       sx = en - es;
       if (t == 0) {
         P.sY[c] = en - ep;
+        P.e_prev[c] = ep;       // the pending exponent before this step (read by a fused J)
         P.e_pend[c] = en;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
       }
@@ -541,7 +590,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   double* xo = p.X + (long long)(valid ? c : 0) * p.ldx + p.t0;
   const long long tstride = (long long)(2 * p.nks) * (kBN * kBK);
   const long long half = (long long)p.nks * (kBN * kBK);
-  double* Wc = P.W + (long long)((valid ? c : 0) / kBN) * tstride + ((valid ? c : 0) % kBN) * 4;
+  double* Wc = p.Wout + (long long)((valid ? c : 0) / kBN) * tstride + ((valid ? c : 0) % kBN) * 4;
 #pragma unroll
   for (int q = 0; q < G; ++q) {
     const int g = (q - rot % G + G) % G;
@@ -570,6 +619,8 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       Wc[off + half] = 0.0;
     }
   }
+  // W is read next by bulk copies (the async proxy): order the generic writes before them
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 template <int G>

@@ -75,6 +75,7 @@ struct DevPlan {
   // robustness state
   int* e_pend;        // per column: exponent of the pending (not yet solved) rows
   int* sY;            // per column: exponent shift of the pending rows at this step
+  int* e_prev;        // per column: pending exponent before the last decision (fused pairs)
   unsigned long long* nY;   // 2 x n_sel: max |pending| (double bits), double buffered
   int* e_seg;         // M x n_sel: exponent of each solved segment
   double* nrm_seg;    // M x n_sel: max(|Re|,|Im|) of the segment
@@ -117,6 +118,11 @@ struct UpdParams {
   unsigned long long* nY_out;
   int vec;           // 16-byte aligned X access possible
   const double* Apk; // S/T panel packed in fragment order (update_packs()), or null
+  int row_lo;        // rows [row_lo, rows) are updated (0, or a tile start for the thin update)
+  // optional second K segment (two-step fused update): S/T columns of tile t0b (nksb chunks
+  // per part) against Wb; nksb = 0 if absent
+  int t0b, nksb;
+  const double* Wb;
 };
 
 // Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.
@@ -137,6 +143,15 @@ struct Diag2Params {
   DevPlan P;
   int nY_in;
   int cpt;                 // columns per warp task (set by launch_diag3)
+  double* Wout;            // where this step's B operand W goes
+  // second step of a fused pair (I, J = I - 1): the update of the rows above tile J is done
+  // once with both tiles; tile I's step left its W in Wprev (nks_prev chunks per part)
+  int fused;
+  int Iprev;               // I
+  int cs_prev;             // columns >= cs_prev were active at step I
+  int zero_pend_end;       // columns < zero_pend_end (tips of I and J) have no pending rows
+  double* Wprev;
+  int nks_prev;
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)

@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int kc = 0; kc < nkc; ++kc) {
     const int s = kc % kStages;
     mbar_wait(&full[s], (kc / kStages) & 1);
+    // release the previous stage only now (see k_update_t)
+    if (lane == 0 && kc >= 1 && kc - 1 + kStages < nkc) mbar_arrive(&empty[(kc - 1) % kStages]);
     const double* a = sA + s * (kBM * kBK);
     const double* b = sB + s * (kBN * kBK);
 #pragma unroll
@@ -168,7 +170,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
@@ -278,7 +279,7 @@ struct UT {
   static constexpr int MINB = (WN == 2) ? 2 : 1;
 };
 
-template <int WN, int BOX>
+template <int WN, int BOX, int MODE = 0>
 __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
     k_update_t(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
                int n_mtiles, int n_tiles) {
@@ -291,10 +292,15 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkc = 2 * p.nks;
+  // MODE 1 (two-step fused update): a second K segment; MODE 2 (thin update): first row row_lo
+  constexpr bool SEG2 = MODE == 1;
+  const int nkca = 2 * p.nks, nkc = nkca + (SEG2 ? 2 * p.nksb : 0);   // K chunks: a, then b
   const int n_ntl = n_tiles / n_mtiles;
-  // W is stored per 64-column block: [ntile64][kc][BK/4][64][4]
-  const long long wtile = (long long)nkc * (kBN * kBK);
+  const int row_lo = (MODE == 2) ? p.row_lo : 0;
+  const int mbase = row_lo & ~1;                         // 16-byte aligned first row pair
+  // W is stored per 64-column block: [ntile64][kc][BK/4][64][4] (per segment)
+  const long long wtile = (long long)nkca * (kBN * kBK);
+  const long long wtileb = (long long)(2 * p.nksb) * (kBN * kBK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -310,16 +316,20 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
     // ---------------- producer: TMA (S/T chunks) + bulk copies (W chunk) ----------------
     if (lane == 0) {
       int g = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile / n_ntl) * kBM;
+      {
+        const int tile = blockIdx.x;
+        const int m0 = mbase + (tile / n_ntl) * kBM;
         const int nb64 = p.ntile0 + (tile % n_ntl) * (C::BN / kBN);   // first 64-column block
         const int nblk = min(C::BN / kBN, p.ntile_end - nb64);         // 64-column blocks present
         for (int kc = 0; kc < nkc; ++kc, ++g) {
           const int s = g % kStages;
           if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
           mbar_expect_tx(&full[s], kABytes + nblk * kBBytes);
-          const CUtensorMap* tm = (kc < p.nks) ? &tmS : &tmT;
-          const int kcol = p.t0 + (kc % p.nks) * kBK;
+          const bool sb = SEG2 && kc >= nkca;              // segment b
+          const int kl = sb ? kc - nkca : kc;              // chunk within its segment
+          const int nks_s = sb ? p.nksb : p.nks;
+          const CUtensorMap* tm = (kl < nks_s) ? &tmS : &tmT;
+          const int kcol = (sb ? p.t0b : p.t0) + (kl % nks_s) * kBK;
           double* a = sA + s * (kBM * kBK);
           if (BOX == 0) {
             // packed panel (k_pack): one 16 KB bulk copy per stage
@@ -331,7 +341,9 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
               tma_load_2d(a + mo * (kBK * BOX), tm, m0 + mo * BOX, kcol, &full[s]);
           }
           for (int q = 0; q < nblk; ++q)
-            bulk_load(sB + s * (C::BN * kBK) + q * (kBN * kBK), p.W + (long long)(nb64 + q) * wtile + (long long)kc * (kBN * kBK),
+            bulk_load(sB + s * (C::BN * kBK) + q * (kBN * kBK),
+                      (sb ? p.Wb + (long long)(nb64 + q) * wtileb : p.W + (long long)(nb64 + q) * wtile) +
+                          (long long)kl * (kBN * kBK),
                       kBBytes, &full[s]);
         }
       }
@@ -343,8 +355,9 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   const int wm = warp / WN, wn = warp % WN;
   const int rq = lane & 3, cq = lane >> 2;
   int g = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int m0 = (tile / n_ntl) * kBM;
+  {
+    const int tile = blockIdx.x;
+    const int m0 = mbase + (tile / n_ntl) * kBM;
     const int n0 = (p.ntile0 + (tile % n_ntl) * (C::BN / kBN)) * kBN;
     double acc[4][8][2];
     // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         acc[ni][mi][1] = 0.0;
         // a pair straddling the last row is loaded whole (row p.rows exists: p.rows < m <=
         // ldx); that accumulator row is never stored nor counted in the column maximum
-        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, ld && (i0 < p.rows));
+        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, ld && (i0 < p.rows) && (i0 + 1 >= row_lo));
       }
     }
 #pragma unroll
@@ -383,6 +396,13 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
     for (int kc = 0; kc < nkc; ++kc, ++g) {
       const int s = g % kStages;
       mbar_wait(&full[s], (g / kStages) & 1);
+      // Release the previous stage only now, not at the end of its own iteration: ptxas may
+      // schedule an mbarrier arrive above the DMMAs of the chunk, i.e. while the last shared-
+      // memory fragment loads are still in flight, and a fast TMA refill of that stage then
+      // races them (observed as run-to-run differences of whole 8-row boxes with K > 16
+      // chunks).  Every DMMA of chunk kc-1 has issued -- its fragments have landed -- before
+      // this point.  (The last kStages chunks have no refill to release.)
+      if (lane == 0 && kc >= 1 && kc - 1 + kStages < nkc) mbar_arrive(&empty[(g - 1) % kStages]);
       const double* a = sA + s * (kBM * kBK);
       const double* b = bw + s * (C::BN * kBK);
 #pragma unroll
@@ -407,7 +427,6 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
 
     // ---------------- epilogue: store Y, per-column max over the next pending rows ----------------
@@ -421,9 +440,11 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
       for (int mi = 0; mi < 8; ++mi) {
         const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
         const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
-        const bool both = cvalid && (i0 + 1 < p.rows);
+        // rows [row_lo, rows) only: a pair may straddle either end
+        const bool both = cvalid && (i0 + 1 < p.rows) && (i0 >= row_lo);
         st2p(xc + i0, v0, v1, both);
-        st1p(xc + i0, v0, cvalid && i0 + 1 == p.rows);
+        st1p(xc + i0, v0, cvalid && i0 + 1 == p.rows && i0 >= row_lo);
+        if (MODE == 2) st1p(xc + i0 + 1, v1, cvalid && i0 + 1 == row_lo && i0 + 1 < p.rows);
         if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
         if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
       }
@@ -452,15 +473,15 @@ int update_version() {
 int update_box_rows() { return update_version() == 3 ? 4 : 8; }
 bool update_packs() { return update_version() == 5; }
 
-template <int WN, int BOX>
+template <int WN, int BOX, int MODE = 0>
 static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
                             cudaStream_t st, int persist) {
   using C = UT<WN, BOX>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_update_t<WN, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_update_t<WN, BOX, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_update_t<WN, BOX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(k_update_t<WN, BOX, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -468,11 +489,14 @@ static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdP
   const int n_ntl = (n_ntiles64 + per - 1) / per;
   p.ntile_end = p.ntile0 + n_ntiles64;
   const int n_tiles = n_mtiles * n_ntl;
-  int grid = n_tiles;
-  if (persist > 0 && grid > persist * g_upd_sms) grid = persist * g_upd_sms;
-  k_update_t<WN, BOX><<<grid, C::THREADS, C::SMEM, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
+  const int grid = n_tiles;   // one tile per CTA (a persistent tile loop measured no faster)
+  (void)persist;
+  k_update_t<WN, BOX, MODE><<<grid, C::THREADS, C::SMEM, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
   return cudaGetLastError();
 }
+
+static cudaError_t launch_update_impl(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
+                                      int n_mtiles, int n_ntiles, cudaStream_t st, int ver, int persist);
 
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st) {
@@ -494,8 +518,17 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
+  return launch_update_impl(tmS, tmT, p, n_mtiles, n_ntiles, st, ver, persist);
+}
+
+static cudaError_t launch_update_impl(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
+                                      int n_mtiles, int n_ntiles, cudaStream_t st, int ver, int persist) {
   // the template kernels move C in 16-byte pairs: X 16-byte aligned with an even ldx
-  if (ver == 2 && p.vec) return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  if (ver == 2 && p.vec) {
+    if (p.nksb > 0) return launch_t<2, 8, 1>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+    if (p.row_lo > 0) return launch_t<2, 8, 2>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+    return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+  }
   if (ver == 3 && p.vec) return launch_t<2, 4>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   if (ver == 4 && p.vec) return launch_t<4, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   if (ver == 5 && p.vec && p.Apk) return launch_t<2, 0>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);

@@ -188,6 +188,20 @@ def test_leading_dimensions_and_alignment(zz):
         assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
 
 
+def test_repeat_bitwise_fused_pairs(zz):
+    # full 128-row tiles: every fused update runs K = 2 x 256 (32 pipeline chunks); repeated
+    # solves and an odd ldx (internal aligned workspace) must give identical bits -- this is
+    # the regression test of the stage-release race of the update pipeline (DESIGN.md s.7)
+    S, T, _ = gen.config("C3", seed=1, m=3000, n2=450)
+    X0, e0, info = solve(zz, S, T, mb=128)
+    assert info["n_tiles"] >= 20 and info["fused_pairs"] >= 9
+    for _ in range(3):
+        X1, e1, _ = solve(zz, S, T, mb=128)
+        assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
+    X2, e2, _ = solve(zz, S, T, mb=128, ldx=3001)
+    assert np.array_equal(X2, X0) and np.array_equal(e2, e0)
+
+
 def test_power_of_two_equivariance_and_prescale(zz):
     S, T, _ = gen.config("C1", seed=6)
     X0, e0, _ = solve(zz, S, T, mb=32)
