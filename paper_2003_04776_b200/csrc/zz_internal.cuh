@@ -123,6 +123,7 @@ struct UpdParams {
   // per part) against Wb; nksb = 0 if absent
   int t0b, nksb;
   const double* Wb;
+  int l2hint;        // L2 eviction priorities: C evict_first, W evict_last (set by launch_update)
 };
 
 // Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.

@@ -225,6 +225,37 @@ __device__ __forceinline__ void st1p(double* p, double x, bool pr) {
                ::"l"(p), "d"(x), "r"((int)pr) : "memory");
 }
 
+// the same with an L2 eviction-priority policy (createpolicy): the C tiles stream through L2
+// once per step (evict_first) while W is re-read by every m-tile of the step (evict_last)
+__device__ __forceinline__ uint64_t l2_policy(bool last, bool on) {
+  uint64_t pol;
+  if (!on)
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  else if (last)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void ld2h(double& x, double& y, const double* p, bool pr, uint64_t pol) {
+  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %4;\n}"
+      : "+d"(x), "+d"(y) : "l"(p), "r"((int)pr), "l"(pol));
+}
+__device__ __forceinline__ void st2h(double* p, double x, double y, bool pr, uint64_t pol) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %4;\n}"
+               ::"l"(p), "d"(x), "d"(y), "r"((int)pr), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st1h(double* p, double x, bool pr, uint64_t pol) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.L2::cache_hint.f64 [%0], %1, %3;\n}"
+               ::"l"(p), "d"(x), "r"((int)pr), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_load_h(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void ld1p_i(int& x, const int* p, bool pr) {
   asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q ld.global.b32 %0, [%1];\n}" : "+r"(x) : "l"(p), "r"((int)pr));
 }
@@ -315,6 +346,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   if (warp == C::CW) {
     // ---------------- producer: TMA (S/T chunks) + bulk copies (W chunk) ----------------
     if (lane == 0) {
+      const uint64_t pol_w = l2_policy(true, p.l2hint & 1);
       int g = 0;
       {
         const int tile = blockIdx.x;
@@ -341,10 +373,10 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
               tma_load_2d(a + mo * (kBK * BOX), tm, m0 + mo * BOX, kcol, &full[s]);
           }
           for (int q = 0; q < nblk; ++q)
-            bulk_load(sB + s * (C::BN * kBK) + q * (kBN * kBK),
-                      (sb ? p.Wb + (long long)(nb64 + q) * wtileb : p.W + (long long)(nb64 + q) * wtile) +
-                          (long long)kl * (kBN * kBK),
-                      kBBytes, &full[s]);
+            bulk_load_h(sB + s * (C::BN * kBK) + q * (kBN * kBK),
+                        (sb ? p.Wb + (long long)(nb64 + q) * wtileb : p.W + (long long)(nb64 + q) * wtile) +
+                            (long long)kl * (kBN * kBK),
+                        kBBytes, &full[s], pol_w);
         }
       }
     }
@@ -354,6 +386,8 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   // ---------------- consumers: 2 (rows) x WN (columns) warps, 64 x 32 each ----------------
   const int wm = warp / WN, wn = warp % WN;
   const int rq = lane & 3, cq = lane >> 2;
+  const uint64_t pol_c = l2_policy(false, p.l2hint & 2);
+  const uint64_t pol_s = l2_policy(false, p.l2hint & 4);
   int g = 0;
   {
     const int tile = blockIdx.x;
@@ -378,7 +412,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         acc[ni][mi][1] = 0.0;
         // a pair straddling the last row is loaded whole (row p.rows exists: p.rows < m <=
         // ldx); that accumulator row is never stored nor counted in the column maximum
-        ld2p(acc[ni][mi][0], acc[ni][mi][1], xc + i0, ld && (i0 < p.rows) && (i0 + 1 >= row_lo));
+        ld2h(acc[ni][mi][0], acc[ni][mi][1], xc + i0, ld && (i0 < p.rows) && (i0 + 1 >= row_lo), pol_c);
       }
     }
 #pragma unroll
@@ -442,9 +476,9 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
         // rows [row_lo, rows) only: a pair may straddle either end
         const bool both = cvalid && (i0 + 1 < p.rows) && (i0 >= row_lo);
-        st2p(xc + i0, v0, v1, both);
-        st1p(xc + i0, v0, cvalid && i0 + 1 == p.rows && i0 >= row_lo);
-        if (MODE == 2) st1p(xc + i0 + 1, v1, cvalid && i0 + 1 == row_lo && i0 + 1 < p.rows);
+        st2h(xc + i0, v0, v1, both, pol_s);
+        st1h(xc + i0, v0, cvalid && i0 + 1 == p.rows && i0 >= row_lo, pol_s);
+        if (MODE == 2) st1h(xc + i0 + 1, v1, cvalid && i0 + 1 == row_lo && i0 + 1 < p.rows, pol_s);
         if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
         if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
       }
@@ -518,7 +552,11 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
     attr = true;
   }
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
-  return launch_update_impl(tmS, tmT, p, n_mtiles, n_ntiles, st, ver, persist);
+  // ZZ_L2HINT (bits): 1 = W evict_last, 2 = C loads evict_first, 4 = C stores evict_first
+  static const int l2hint = getenv("ZZ_L2HINT") ? atoi(getenv("ZZ_L2HINT")) : 7;
+  UpdParams q = p;
+  q.l2hint = l2hint;
+  return launch_update_impl(tmS, tmT, q, n_mtiles, n_ntiles, st, ver, persist);
 }
 
 static cudaError_t launch_update_impl(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
