@@ -210,6 +210,8 @@ def main():
     ap.add_argument("--cpu-blocks", type=int, default=192)
     ap.add_argument("--ref-blocks", type=int, default=24)
     ap.add_argument("--nb", type=int, default=64, help="column-block width of the multi-GPU shard")
+    ap.add_argument("--back", action="store_true",
+                    help="also time zz_tgevc_back (back-transformation W = V X, xTGEVC HOWMNY='B')")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -373,6 +375,39 @@ def main():
             err.append(np.linalg.norm(a - b) / np.linalg.norm(b))
         res["parity_sample"] = {"columns": int(len(cols)), "max_rel_2norm": float(max(err)),
                                 "median": float(np.median(err)), "tolerance": 1e-10}
+    if rank == 0 and world == 1 and args.back:
+        # back-transformation leg (a separate capability, not part of the headline metric):
+        # V is a seeded Gaussian N(0, 1/m) made on the device -- the work does not depend on
+        # V being orthogonal; the product is the DGEMM column blocks of zz_tgevc_back
+        Xd = Xd_check = None
+        torch.cuda.empty_cache()
+        gv = torch.Generator(device=dev)
+        gv.manual_seed(args.seed + 7)
+        Vd = torch.randn((m, m), generator=gv, dtype=torch.float64, device=dev).t() * (1.0 / np.sqrt(m))
+        Wd = zz.empty_colmajor(m, m, device=dev)
+        F_back = float(sum(sz * 2.0 * m * (j + sz) for j, sz in blocks))
+        for _ in range(2):
+            zz.tgevc_back(Sd, Td, Vd, W=Wd, col_scale_exp=Ed)
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        kb = max(1, args.steps)
+        ms_back = 0.0
+        b0.record(st)
+        for _ in range(kb):
+            zz.tgevc_back(Sd, Td, Vd, W=Wd, col_scale_exp=Ed)
+            ms_back += zz.last_info()["ms_back"]
+        b1.record(st)
+        torch.cuda.synchronize()
+        tb = b0.elapsed_time(b1) / 1e3 / kb
+        ms_back /= kb
+        res["backtransform"] = {
+            "api": "zz_tgevc_back (solve + W = V X in 256-column DGEMM blocks with K = 1 + max r_c + LAPACK normalisation)",
+            "seconds_per_step": tb, "ms_back": ms_back, "flops_back": F_back,
+            "tflops_back": F_back / (ms_back * 1e-3) * 1e-12,
+            "frac_of_dgemm_peak": F_back / (ms_back * 1e-3) * 1e-12 / 35.5,
+            "dgemm_peak_source": "cuBLAS DGEMM 8192^3 measured 35.5 TFLOP/s (profiles/r01_fp64_peak.json)",
+            "V": "seeded Gaussian N(0, 1/m) on the device (timing only)"}
     if rank == 0:
         emit(res)
     if world > 1:

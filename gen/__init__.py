@@ -73,3 +73,15 @@ def config(name, seed=0, **kw):
     c = dict(CONFIGS[name])
     c.update(kw)
     return generate(seed=seed, **c)
+
+
+def orthogonal(m, seed=0):
+    """Seeded random orthogonal m x m matrix (column-major): the Q factor of a Gaussian
+    matrix with the signs of R's diagonal folded in (Haar-distributed).  Stands in for the
+    Schur vectors of the QZ step (the back-transformation input, include/zz.h zz_tgevc_back)."""
+    rng = np.random.default_rng(1000003 + seed)
+    G = rng.standard_normal((m, m))
+    Q, R = np.linalg.qr(G)
+    d = np.sign(np.diag(R))
+    d[d == 0] = 1.0
+    return np.asfortranarray(Q * d)

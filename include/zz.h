@@ -66,6 +66,7 @@ typedef struct zz_info {
   double ms_steps;         /* the wavefront (diagonal solves + updates) */
   double ms_normalize;     /* consistency and normalisation */
   double ms_update;        /* summed device time of the robust-update kernels (if timed) */
+  double ms_back;          /* zz_tgevc_back: back-transformation GEMMs + normalisation */
 } zz_info_t;
 
 /* Create (or re-bind) this thread's context on CUDA device `device`.
@@ -116,6 +117,28 @@ int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const in
  * Arguments and status codes as zz_tgevc. */
 int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select,
                   double* X, int ldx, int* col_scale_exp);
+
+/* zz_tgevc_back: back-transformed eigenvectors, the xTGEVC HOWMNY='B' mode (PAPER.md:28-32:
+ * with S = U^T A V and T = U^T B V from the QZ step, S z = lambda T z implies
+ * A (V z) = lambda B (V z); the back-transform uses V, not U).
+ *   m, S, lds, T, ldt, select   as zz_tgevc                                 [args 1-6]
+ *   V, ldv         DEVICE, m x m column-major, ldv >= max(1,m); never written
+ *                  (the right Schur vectors; any real matrix is accepted)     [args 7,8]
+ *   W, ldw         DEVICE, m x n_sel column-major, ldw >= max(1,m); written
+ *                  completely: W(:,c) = V(:, 0:r_c) X(0:r_c, c) with X the
+ *                  zz_tgevc result of column c (r_c its last row), then
+ *                  normalised as LAPACK does after its back-transform:
+ *                  max_i |w_i| = 1 (real), max_i (|Re w_i| + |Im w_i|) = 1 (pair).
+ *                  W must not overlap V, S or T.                              [args 9,10]
+ *   col_scale_exp  DEVICE int32[n_sel] or NULL: as zz_tgevc (the exponents of the
+ *                  (S,T) eigenvectors before their normalisation)             [arg 11]
+ * The product runs as column blocks of 256 columns with K = 1 + the block's largest r_c
+ * (cuBLAS DGEMM: X is block-upper-triangular, so the work is ~ m^3 flop for all
+ * eigenvectors instead of 2 m^3); normalisation is one pass over W.  The library keeps an
+ * m x n_sel workspace for X.  Status codes as zz_tgevc; -100 also covers a cuBLAS error.
+ */
+int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+                  const double* V, int ldv, double* W, int ldw, int* col_scale_exp);
 
 /* Number of output columns zz_tgevc would produce for (S, select) with S on the HOST
  * (pairs count 2).  Returns n_sel >= 0, -105, or -i for a bad argument.  Host-only. */

@@ -128,3 +128,35 @@ def tgevc(S, T, select=None, protect=True, nthreads=0):
                           e.ctypes.data, L.ctypes.data, pairs.ctypes.data, stats.ctypes.data,
                           1 if protect else 0, nthreads)
     return dict(X=X[:, :n], e=e[:n], logmax=L[:n], pairs=pairs[:m], stats=stats, status=st)
+
+
+def tgevc_back(S, T, V, select=None):
+    """Back-transformed eigenvectors (xTGEVC HOWMNY='B'; PAPER.md:28-32 read with SURVEY.md A1:
+    A (V z) = lambda B (V z) for S = U^T A V, T = U^T B V): W(:, c) = V X(:, c) with X from
+    tgevc() above, then LAPACK's normalisation of back-transformed vectors: max |w_i| = 1
+    for a real column, max (|Re w_i| + |Im w_i|) = 1 for a complex pair (multiplied by the
+    reciprocal of the maximum).  Plain numpy matmul; pinned against LAPACKE_dtgevc with
+    HOWMNY='B' (tests/test_oracle_vectors.py)."""
+    S, T, V = _f(S), _f(T), _f(V)
+    m = S.shape[0]
+    r = tgevc(S, T, select=select)
+    if r["status"] != 0:
+        return dict(W=None, status=r["status"])
+    X = r["X"]
+    W = np.asfortranarray(V @ X)
+    bs, bz = blocks(S)
+    sel = _sel(select, m)
+    col = 0
+    for j, sz in zip(bs, bz):
+        if sel is not None and not (sel[j] or (sz == 2 and sel[j + 1])):
+            continue
+        if sz == 1:
+            mx = np.max(np.abs(W[:, col])) if m else 0.0
+            if mx > 0:
+                W[:, col] *= 1.0 / mx
+        else:
+            mx = np.max(np.abs(W[:, col]) + np.abs(W[:, col + 1]))
+            if mx > 0:
+                W[:, col:col + 2] *= 1.0 / mx
+        col += sz
+    return dict(W=W, X=X, e=r["e"], pairs=r["pairs"], status=0)

@@ -27,7 +27,7 @@ STATUS = {
     -106: "unsupported tile size",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host",
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -46,7 +46,8 @@ class Info(ctypes.Structure):
                 ("update_launches", ctypes.c_int), ("total_launches", ctypes.c_int),
                 ("fused_pairs", ctypes.c_int), ("reserved", ctypes.c_int),
                 ("ms_setup", ctypes.c_double), ("ms_steps", ctypes.c_double),
-                ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double)]
+                ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double),
+                ("ms_back", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -79,6 +80,7 @@ def load(build_if_missing=True):
         "zz_set_timing": ([ci], ci),
         "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
+        "zz_tgevc_back": ([ci, vp, ci, vp, ci, vp, vp, ci, vp, ci, vp], ci),
         "zz_count_columns": ([ci, vp, ci, vp], ci),
         "zz_partition": ([ci, vp, ci, vp], ci),
         "zz_last_info": ([ctypes.POINTER(Info)], ci),
@@ -223,6 +225,46 @@ def tgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None, n_sel=None
                      col_scale_exp.data_ptr() if n_sel > 0 else None)
     _check(r, "zz_tgevc")
     return X, col_scale_exp
+
+
+def tgevc_back(S, T, V, select=None, W=None, col_scale_exp=None, stream=None, n_sel=None):
+    """Back-transformed eigenvectors W = V X (xTGEVC HOWMNY='B'; include/zz.h zz_tgevc_back).
+
+    S, T, V: CUDA float64 column-major m x m tensors (V: the right Schur vectors of the QZ
+    step, A = U S V^T, B = U T V^T); never written.  Returns (W, col_scale_exp), W m x n_sel
+    column-major, each column (pair) normalised to max |w| = 1 (max |Re| + |Im| = 1)."""
+    import torch
+    lib = load()
+    m = S.shape[0]
+    if not (S.is_cuda and T.is_cuda and V.is_cuda):
+        raise ValueError("S, T and V must be CUDA tensors (no CPU fallback)")
+    if S.dtype != torch.float64 or T.dtype != torch.float64 or V.dtype != torch.float64:
+        raise ValueError("S, T and V must be float64")
+    dev = S.device.index
+    if dev not in _inited:
+        init(dev)
+    lds = _ld_colmajor(S, m, "S")
+    ldt = _ld_colmajor(T, m, "T")
+    ldv = _ld_colmajor(V, m, "V")
+    sel = _sel_array(select, m)
+    if n_sel is None:
+        if sel is None:
+            n_sel = m
+        else:
+            sub = torch.diagonal(S, -1).cpu().numpy() if m > 1 else []
+            n_sel = _count_from_sub(sub, m, sel)
+    if W is None:
+        W = empty_colmajor(m, max(n_sel, 1), device=S.device)[:, :n_sel]
+    ldw = _ld_colmajor(W, m, "W") if n_sel > 0 else max(m, 1)
+    if col_scale_exp is None:
+        col_scale_exp = torch.empty(max(n_sel, 1), dtype=torch.int32, device=S.device)[:n_sel]
+    st = stream if stream is not None else torch.cuda.current_stream(S.device)
+    _check(lib.zz_set_stream(ctypes.c_void_p(st.cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc_back(m, S.data_ptr(), lds, T.data_ptr(), ldt, None if sel is None else sel.ctypes.data,
+                          V.data_ptr(), ldv, W.data_ptr() if n_sel > 0 else ctypes.c_void_p(1), ldw,
+                          col_scale_exp.data_ptr() if n_sel > 0 else None)
+    _check(r, "zz_tgevc_back")
+    return W, col_scale_exp
 
 
 def _count_from_sub(sub, m, sel):

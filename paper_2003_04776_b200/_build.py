@@ -8,7 +8,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libzz.so")
-SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu"]
+SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu", "zz_back.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -44,8 +44,10 @@ def build(force=False, verbose=False):
             raise RuntimeError("nvcc failed on %s:\n%s%s" % (src, r.stdout, r.stderr))
         log.append(r.stderr)
     objs = [obj for _, obj, _ in results]
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
     r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO + ".tmp"] + objs
-                      , capture_output=True, text=True)
+                       + ["-L" + cudalib, "-lcublas", "-Xlinker", "-rpath", "-Xlinker", cudalib],
+                       capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     if verbose:

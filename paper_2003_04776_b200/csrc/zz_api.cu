@@ -7,6 +7,7 @@
 // row I for every active eigenvector (tips for the blocks inside tile I), then one fused
 // robust update of all rows above it.  Two host synchronisations happen before the
 // wavefront (structure, then pair/norm status); none inside it.
+#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -61,6 +62,9 @@ struct Context {
   // workspace
   Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, status, tmp, Sc, Tc, Apk, Xi;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
+  Buf Xb;              // X of zz_tgevc_back
+  cublasHandle_t blas = nullptr;          // the back-transformation GEMMs
+  std::vector<int> last_col_r;            // r_c of the last call's columns (host)
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> ev_copy;       // per-panel arrival events of zz_tgevc_host
   cudaStream_t copy = nullptr;            // host-to-device copy stream of zz_tgevc_host
@@ -71,6 +75,9 @@ struct Context {
     Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W, &W2,
                   &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
+    Xb.release();
+    if (blas) cublasDestroy(blas);
+    blas = nullptr;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
     for (cudaEvent_t e : ev_copy) cudaEventDestroy(e);
@@ -231,6 +238,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     n_sel += bz[p];
   }
   info.n_sel = n_sel;
+  c->last_col_r = col_r;
   const int n_items = (int)item_col.size();
   std::vector<int> tile_item((size_t)M + 1, n_items), cs((size_t)M + 1, n_sel);
   for (int I = M - 1; I >= 0; --I) {
@@ -646,6 +654,43 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   return 0;
 }
 
+// xTGEVC HOWMNY='B' (reading A1): W = V X, column block by column block with
+// K = 1 + the block's largest r_c (columns are in block order, so r_c is non-decreasing and
+// X is zero below r_c), then LAPACK's normalisation of the back-transformed columns.
+int tgevc_back_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
+                      const int* select, const double* V, long long ldv, double* W, long long ldw, int* cse) {
+  cudaStream_t st = c->stream;
+  const long long ldxb = (m + 1) & ~1LL;
+  CK(c->Xb.ensure(sizeof(double) * (size_t)ldxb * (size_t)std::max(m, 1)));
+  double* Xb = c->Xb.as<double>();
+  int r = tgevc_device(c, m, S, lds, T, ldt, select, Xb, ldxb, cse);
+  if (r) return r;
+  const int n_sel = c->info.n_sel;
+  if (n_sel == 0) return 0;
+  if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  if (cublasSetStream(c->blas, st) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  if (cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  CK(cudaEventRecord(c->e0, st));
+  const double one = 1.0, zero = 0.0;
+  const int nbk = 256;
+  for (int c0 = 0; c0 < n_sel; c0 += nbk) {
+    const int nc = std::min(nbk, n_sel - c0);
+    const int K = c->last_col_r[c0 + nc - 1] + 1;
+    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, nc, K, &one, V, (int)ldv, Xb + (size_t)c0 * ldxb,
+                    (int)ldxb, &zero, W + (size_t)c0 * ldw, (int)ldw) != CUBLAS_STATUS_SUCCESS)
+      return ZZ_ERR_CUDA;
+  }
+  // the column kinds of the last call are still in the workspace (DevPlan.col_kind)
+  CK(launch_back_norm(W, ldw, m, n_sel, c->coli.as<int>(), st));
+  CK(cudaEventRecord(c->e1, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->e0, c->e1);
+  c->info.ms_back = ms;
+  c->info.total_launches += 1;
+  return 0;
+}
+
 int check_args(int m, const double* S, int lds, const double* T, int ldt, double* X, int ldx) {
   if (m < 0) return -1;
   if (m > 0 && !S) return -2;
@@ -708,6 +753,22 @@ int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const in
     return 0;
   }
   return tgevc_device(g_ctx, m, S, lds, T, ldt, select, X, ldx, col_scale_exp);
+}
+
+int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+                  const double* V, int ldv, double* W, int ldw, int* col_scale_exp) {
+  int a = check_args(m, S, lds, T, ldt, W, ldw);
+  if (a == -7 || a == -8) a -= 2;     // W, ldw are arguments 9 and 10
+  if (a) return a;
+  if (m > 0 && !V) return -7;
+  if (ldv < std::max(1, m)) return -8;
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (cudaSetDevice(g_ctx->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (m == 0) {
+    memset(&g_ctx->info, 0, sizeof(g_ctx->info));
+    return 0;
+  }
+  return tgevc_back_device(g_ctx, m, S, lds, T, ldt, select, V, ldv, W, ldw, col_scale_exp);
 }
 
 int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,

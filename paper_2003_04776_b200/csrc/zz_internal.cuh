@@ -183,5 +183,7 @@ size_t pack_bytes(int rows, int nks);
 cudaError_t launch_pack(const double* S, long long lds, const double* T, long long ldt, int rows, int t0, int nt,
                         int nks, double* Apk, cudaStream_t st);
 int update_box_rows();   // rows per TMA box of the S/T tensor maps
+// zz_back.cu: LAPACK normalisation of the back-transformed columns (xTGEVC HOWMNY='B')
+cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const int* col_kind, cudaStream_t st);
 
 }  // namespace zz

@@ -43,3 +43,23 @@ def dtgevc(S, T, select=None):
               T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), 1, VR.ctypes.data_as(vp), m, m,
               ctypes.byref(mo))
     return info, VR[:, :mo.value]
+
+
+def dtgevc_back(S, T, V):
+    """Back-transformed right eigenvectors (HOWMNY='B', VR = V on entry); returns (info, VR)."""
+    global _f
+    if _f is None:
+        lib = ctypes.CDLL(_paths()[0])
+        _f = lib.scipy_LAPACKE_dtgevc
+        _f.restype = ctypes.c_int
+    S = np.asfortranarray(S, dtype=np.float64)
+    T = np.asfortranarray(T, dtype=np.float64)
+    m = S.shape[0]
+    VR = np.array(V, dtype=np.float64, order="F", copy=True)
+    VL = np.zeros((1, 1))
+    mo = ctypes.c_int(0)
+    vp = ctypes.c_void_p
+    info = _f(102, ctypes.c_char(b"R"), ctypes.c_char(b"B"), None, m, S.ctypes.data_as(vp), m,
+              T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), 1, VR.ctypes.data_as(vp), m, m,
+              ctypes.byref(mo))
+    return info, VR[:, :mo.value]

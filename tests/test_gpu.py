@@ -408,3 +408,55 @@ def test_host_path_select_ld_errors_and_prescale(zz):
     X2, e2, info = _host_solve(zz, np.asfortranarray(np.ldexp(S2, 1021)), np.asfortranarray(np.ldexp(T2, 1021)), 32)
     assert info["prescaled"] == 1
     assert np.array_equal(X2, Xr)
+
+
+# ---- back-transformation W = V X (xTGEVC HOWMNY='B', include/zz.h zz_tgevc_back) ----
+
+def _back(zz, S, T, V, mb=0, select=None, ldw=None):
+    zz.set_tile(mb)
+    m = S.shape[0]
+    n = oracle.count_columns(S, select)
+    Sd, Td, Vd = to_dev(S), to_dev(T), to_dev(V)
+    W = None
+    if ldw is not None:
+        W = torch.full((max(n, 1), ldw), np.nan, dtype=torch.float64, device="cuda").t()[:m, :n]
+    W, e = zz.tgevc_back(Sd, Td, Vd, select=select, W=W, n_sel=n)
+    torch.cuda.synchronize()
+    return W.cpu().numpy(), e.cpu().numpy(), zz.last_info()
+
+
+@pytest.mark.parametrize("name,seed,mb", [("C1", 0, 32), ("C1", 1, 64), ("C1", 5, 32), ("C2", 0, 128), ("C2", 1, 64)])
+def test_back_parity(zz, name, seed, mb):
+    S, T, _ = gen.config(name, seed=seed)
+    V = gen.orthogonal(S.shape[0], seed=seed)
+    W, e, info = _back(zz, S, T, V, mb=mb)
+    ref = oracle.tgevc_back(S, T, V)
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(W, ref["W"], lay)
+    assert np.isfinite(W).all() and info["ms_back"] > 0
+    assert ali.max() <= TOL and raw.max() <= TOL, (ali.max(), raw.max())
+    for col, j, sz in lay:       # LAPACK normalisation of the back-transformed columns
+        w = np.abs(W[:, col]) if sz == 1 else np.abs(W[:, col]) + np.abs(W[:, col + 1])
+        assert abs(w.max() - 1.0) <= 4 * 2.0 ** -53
+
+
+def test_back_select_ldw_and_residual(zz):
+    S, T, _ = gen.config("C2", seed=2, m=700, n2=105)
+    m = S.shape[0]
+    V = gen.orthogonal(m, seed=3)
+    Q = gen.orthogonal(m, seed=4)
+    W0, e0, _ = _back(zz, S, T, V, mb=64)
+    W1, e1, _ = _back(zz, S, T, V, mb=64, ldw=703)        # odd ldw: bitwise the same
+    assert np.array_equal(W0, W1) and np.array_equal(e0, e1)
+    sel = np.zeros(m, np.int32)
+    sel[::7] = 1
+    Ws, es, _ = _back(zz, S, T, V, mb=64, select=sel)
+    lay_f = checks.column_layout(None, None, S)
+    lay_s = checks.column_layout(None, None, S, sel)
+    start = {j: col for col, j, _ in lay_f}
+    for col, j, sz in lay_s:      # a selected column is the full solve's column, bit for bit
+        assert np.array_equal(Ws[:, col:col + sz], W0[:, start[j]:start[j] + sz])
+    # residual on the original pencil A = Q S V^T, B = Q T V^T
+    ref = oracle.tgevc(S, T)
+    D, Bm, _ = checks.build_DB(ref["pairs"], S)
+    assert checks.residual(Q @ S @ V.T, Q @ T @ V.T, W0, D, Bm) <= 10 * m * 2.0 ** -53

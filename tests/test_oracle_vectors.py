@@ -305,3 +305,61 @@ def test_stress_c5_recipe_small_scale():
     assert np.isfinite(r["X"]).all() and (r["e"] <= 0).all()
     rn = oracle.tgevc(S, T, protect=False)
     assert (~np.isfinite(rn["X"]).all(axis=0)).sum() > 0
+
+
+# ---- back-transformation (xTGEVC HOWMNY='B'; include/zz.h zz_tgevc_back) ----
+
+@pytest.mark.parametrize("seed", range(5))
+def test_lapack_dtgevc_back_C1(seed):
+    # LAPACK's own back-transform (VR = V on entry) pins oracle.tgevc_back: the product
+    # V X and the normalisation of the back-transformed columns
+    _lapack_or_skip()
+    S, T, _ = gen.config("C1", seed=seed)
+    V = gen.orthogonal(S.shape[0], seed=seed)
+    r = oracle.tgevc_back(S, T, V)
+    info, VR = lapack_pin.dtgevc_back(S, T, V)
+    assert info == 0 and r["status"] == 0
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(r["W"], VR, lay)
+    assert ali.max() < 1e-11 and raw.max() < 1e-11, (ali.max(), raw.max())
+
+
+def test_back_identity_V_is_the_plain_result():
+    # V = I: the back-transform of the normalised X is X again, up to the renormalisation
+    # (X's maximum is 1 within one rounding, R11: each entry moves by at most 2 ulps)
+    S, T, _ = gen.config("C1", seed=2)
+    r0 = oracle.tgevc(S, T)
+    r = oracle.tgevc_back(S, T, np.eye(S.shape[0], order="F"))
+    assert np.all(np.abs(r["W"] - r0["X"]) <= 4 * 2.0 ** -53 * np.abs(r0["X"]))
+
+
+def test_back_residual_on_the_original_pencil():
+    # A = Q S V^T, B = Q T V^T: the back-transformed W solves A W D = B W Bm
+    m = 300
+    S, T, _ = gen.generate(m, 45, 1.0 / m, seed=11, gap_mode=2, gap=1e-4)
+    V = gen.orthogonal(m, seed=1)
+    Q = gen.orthogonal(m, seed=2)
+    A, B = Q @ S @ V.T, Q @ T @ V.T
+    r = oracle.tgevc_back(S, T, V)
+    D, Bm, lay = checks.build_DB(r["pairs"], S)
+    assert checks.residual(A, B, r["W"], D, Bm) <= 10 * m * 2.0 ** -53
+    # normalisation: max |w| = 1 (real), max |Re| + |Im| = 1 (pair), to one rounding
+    for col, j, sz in lay:
+        w = np.abs(r["W"][:, col]) if sz == 1 else np.abs(r["W"][:, col]) + np.abs(r["W"][:, col + 1])
+        assert abs(w.max() - 1.0) <= 2 * 2.0 ** -53
+
+
+def test_back_selected_subset_matches_full_columns():
+    # a selected column's back-transform is the full solve's column (column independence)
+    S, T, _ = gen.config("C1", seed=4)
+    m = S.shape[0]
+    V = gen.orthogonal(m, seed=4)
+    full = oracle.tgevc_back(S, T, V)
+    sel = np.zeros(m, np.int32)
+    sel[[1, 10, 11, 50, 95]] = 1
+    sub = oracle.tgevc_back(S, T, V, select=sel)
+    lay_f = checks.column_layout(None, None, S)
+    lay_s = checks.column_layout(None, None, S, sel)
+    start = {j: col for col, j, _ in lay_f}
+    for col, j, sz in lay_s:
+        assert np.array_equal(sub["W"][:, col:col + sz], full["W"][:, start[j]:start[j] + sz])
