@@ -210,6 +210,7 @@ def main():
     ap.add_argument("--cpu-blocks", type=int, default=192)
     ap.add_argument("--ref-blocks", type=int, default=24)
     ap.add_argument("--nb", type=int, default=64, help="column-block width of the multi-GPU shard")
+    ap.add_argument("--left", action="store_true", help="also time zz_tgevc_left (left eigenvectors)")
     ap.add_argument("--back", action="store_true",
                     help="also time zz_tgevc_back (back-transformation W = V X, xTGEVC HOWMNY='B')")
     args = ap.parse_args()
@@ -375,6 +376,26 @@ def main():
             err.append(np.linalg.norm(a - b) / np.linalg.norm(b))
         res["parity_sample"] = {"columns": int(len(cols)), "max_rel_2norm": float(max(err)),
                                 "median": float(np.median(err)), "tolerance": 1e-10}
+    if rank == 0 and world == 1 and args.left:
+        # left eigenvectors (xTGEVC SIDE='L'): flip-transpose of S and T, the robust right
+        # solve on the flipped pencil, gather back -- same F
+        Yd = zz.empty_colmajor(m, m, device=dev)
+        for _ in range(2):
+            zz.tgevc_left(Sd, Td, Y=Yd, col_scale_exp=Ed)
+        torch.cuda.synchronize()
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        kl = max(1, args.steps)
+        l0.record(st)
+        for _ in range(kl):
+            zz.tgevc_left(Sd, Td, Y=Yd, col_scale_exp=Ed)
+        l1.record(st)
+        torch.cuda.synchronize()
+        tl = l0.elapsed_time(l1) / 1e3 / kl
+        res["left"] = {"api": "zz_tgevc_left (J S^T J flip + robust blocked right solve + gather)",
+                       "seconds_per_step": tl, "value": F / tl * 1e-12, "unit": "TFLOP/s"}
+        Yd = None
+        torch.cuda.empty_cache()
     if rank == 0 and world == 1 and args.back:
         # back-transformation leg (a separate capability, not part of the headline metric):
         # V is a seeded Gaussian N(0, 1/m) made on the device -- the work does not depend on

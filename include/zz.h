@@ -140,6 +140,21 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
 int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, const int* select,
                   const double* V, int ldv, double* W, int ldw, int* col_scale_exp);
 
+/* zz_tgevc_left: selected LEFT eigenvectors y, y^H S = lambda y^H T (PAPER.md:330 names them
+ * as the next step; LAPACK xTGEVC SIDE='L' conventions).  Arguments as zz_tgevc, with
+ *   Y, ldy         DEVICE, m x n_sel column-major; written completely.  Column order, pair
+ *                  layout (Re y, Im y for the eigenvalue with positive imaginary part) and
+ *                  normalisation (max |y| = 1, pairs max |Re|+|Im| = 1) as zz_tgevc; y_i = 0
+ *                  exactly above the eigenvalue's block (rows < its first row).  [args 7,8]
+ *   col_scale_exp  as zz_tgevc, for the left vectors before normalisation.       [arg 9]
+ * Method: (beta S^T - conj(alpha) T^T) y = 0; with the reversal J, (J S^T J, J T^T J) is a real
+ * Schur pencil with the same eigenvalues, and J conj(y) is its right eigenvector, which the
+ * robust blocked path computes (csrc/zz_left.cu: one tiled flip-transpose of each matrix
+ * into a library workspace of 2 m^2 doubles, the solve, one gather back).  A status +j
+ * refers to rows of S.  Ownership and errors as zz_tgevc. */
+int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+                  double* Y, int ldy, int* col_scale_exp);
+
 /* Number of output columns zz_tgevc would produce for (S, select) with S on the HOST
  * (pairs count 2).  Returns n_sel >= 0, -105, or -i for a bad argument.  Host-only. */
 int zz_count_columns(int m, const double* S_host, int lds, const int* select);

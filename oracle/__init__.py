@@ -160,3 +160,41 @@ def tgevc_back(S, T, V, select=None):
                 W[:, col:col + 2] *= 1.0 / mx
         col += sz
     return dict(W=W, X=X, e=r["e"], pairs=r["pairs"], status=0)
+
+
+def tgevc_left(S, T, select=None):
+    """Left eigenvectors y^H S = lambda y^H T (LAPACK xTGEVC SIDE='L').
+    Definition used: y^H (beta S - alpha T) = 0  <=>  (beta S^T - conj(alpha) T^T) y = 0; with J
+    the reversal, (J S^T J, J T^T J) is a real Schur pencil with the same eigenvalues and
+    J conj(y) its right eigenvector for lambda, which tgevc() above computes.  Columns are
+    returned in S's block order, a pair as (Re y, Im y) for the eigenvalue with b > 0,
+    normalised as the right vectors.  Pinned against LAPACKE_dtgevc(SIDE='L') and the
+    left residual (tests/test_oracle_vectors.py)."""
+    S, T = _f(S), _f(T)
+    m = S.shape[0]
+    Sf = np.asfortranarray(S.T[::-1, ::-1])
+    Tf = np.asfortranarray(T.T[::-1, ::-1])
+    sel = _sel(select, m)
+    self_ = None if sel is None else sel[::-1].copy()
+    r = tgevc(Sf, Tf, select=self_)
+    if r["status"] != 0:
+        st = r["status"]
+        return dict(Y=None, status=(m - st) if st > 0 else st)
+    Xf = r["X"]
+    n = Xf.shape[1]
+    bs, bz = blocks(Sf)
+    kinds = []
+    for j, sz in zip(bs, bz):
+        if self_ is not None and not (self_[j] or (sz == 2 and self_[j + 1])):
+            continue
+        kinds += [0] if sz == 1 else [1, 2]
+    Y = np.zeros((m, n), order="F")
+    e = np.zeros(n, np.int32)
+    for c in range(n):
+        cc = n - 1 - c
+        k = kinds[cc]
+        src = cc - 1 if k == 2 else (cc + 1 if k == 1 else cc)
+        sg = -1.0 if k == 1 else 1.0
+        Y[:, c] = sg * Xf[::-1, src]
+        e[c] = r["e"][src]
+    return dict(Y=Y, e=e, pairs=r["pairs"][::-1].copy(), status=0)

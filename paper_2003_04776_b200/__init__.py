@@ -27,7 +27,7 @@ STATUS = {
     -106: "unsupported tile size",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back",
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -81,6 +81,7 @@ def load(build_if_missing=True):
         "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_back": ([ci, vp, ci, vp, ci, vp, vp, ci, vp, ci, vp], ci),
+        "zz_tgevc_left": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_count_columns": ([ci, vp, ci, vp], ci),
         "zz_partition": ([ci, vp, ci, vp], ci),
         "zz_last_info": ([ctypes.POINTER(Info)], ci),
@@ -225,6 +226,42 @@ def tgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None, n_sel=None
                      col_scale_exp.data_ptr() if n_sel > 0 else None)
     _check(r, "zz_tgevc")
     return X, col_scale_exp
+
+
+def tgevc_left(S, T, select=None, Y=None, col_scale_exp=None, stream=None, n_sel=None):
+    """Selected LEFT eigenvectors y^H S = lambda y^H T (LAPACK xTGEVC SIDE='L'; include/zz.h
+    zz_tgevc_left).  Arguments and result layout as tgevc()."""
+    import torch
+    lib = load()
+    m = S.shape[0]
+    if not (S.is_cuda and T.is_cuda):
+        raise ValueError("S and T must be CUDA tensors (no CPU fallback)")
+    if S.dtype != torch.float64 or T.dtype != torch.float64:
+        raise ValueError("S and T must be float64")
+    dev = S.device.index
+    if dev not in _inited:
+        init(dev)
+    lds = _ld_colmajor(S, m, "S")
+    ldt = _ld_colmajor(T, m, "T")
+    sel = _sel_array(select, m)
+    if n_sel is None:
+        if sel is None:
+            n_sel = m
+        else:
+            sub = torch.diagonal(S, -1).cpu().numpy() if m > 1 else []
+            n_sel = _count_from_sub(sub, m, sel)
+    if Y is None:
+        Y = empty_colmajor(m, max(n_sel, 1), device=S.device)[:, :n_sel]
+    ldy = _ld_colmajor(Y, m, "Y") if n_sel > 0 else max(m, 1)
+    if col_scale_exp is None:
+        col_scale_exp = torch.empty(max(n_sel, 1), dtype=torch.int32, device=S.device)[:n_sel]
+    st = stream if stream is not None else torch.cuda.current_stream(S.device)
+    _check(lib.zz_set_stream(ctypes.c_void_p(st.cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc_left(m, S.data_ptr(), lds, T.data_ptr(), ldt, None if sel is None else sel.ctypes.data,
+                          Y.data_ptr() if n_sel > 0 else ctypes.c_void_p(1), ldy,
+                          col_scale_exp.data_ptr() if n_sel > 0 else None)
+    _check(r, "zz_tgevc_left")
+    return Y, col_scale_exp
 
 
 def tgevc_back(S, T, V, select=None, W=None, col_scale_exp=None, stream=None, n_sel=None):

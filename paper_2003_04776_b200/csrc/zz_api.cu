@@ -62,7 +62,8 @@ struct Context {
   // workspace
   Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, status, tmp, Sc, Tc, Apk, Xi;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
-  Buf Xb;              // X of zz_tgevc_back
+  Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
+  Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
   cublasHandle_t blas = nullptr;          // the back-transformation GEMMs
   std::vector<int> last_col_r;            // r_c of the last call's columns (host)
   std::vector<cudaEvent_t> ev;
@@ -76,6 +77,9 @@ struct Context {
                   &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     Xb.release();
+    Sl.release();
+    Tl.release();
+    El.release();
     if (blas) cublasDestroy(blas);
     blas = nullptr;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -691,6 +695,40 @@ int tgevc_back_device(Context* c, int m, const double* S, long long lds, const d
   return 0;
 }
 
+// Left eigenvectors (LAPACK xTGEVC SIDE='L'): y^H (beta S - alpha T) = 0
+// is (beta S^T - conj(alpha) T^T) y = 0, and with the reversal J, (S', T') = (J S^T J, J T^T J) is
+// a real Schur pencil with the same eigenvalues whose right eigenvector for lambda is
+// conj(J y) (csrc/zz_left.cu).  The robust blocked right solve runs on (S', T'); the result
+// is mapped back: rows reversed, a pair's imaginary column negated, columns in S's block order.
+int tgevc_left_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
+                      const int* select, double* Y, long long ldy, int* cse) {
+  cudaStream_t st = c->stream;
+  const long long ldf = (m + 1) & ~1LL;
+  const size_t mat = sizeof(double) * (size_t)ldf * (size_t)m;
+  CK(c->Sl.ensure(mat));
+  CK(c->Tl.ensure(mat));
+  CK(c->Xb.ensure(mat));
+  CK(c->El.ensure(sizeof(int) * (size_t)m));
+  double* Sf = c->Sl.as<double>();
+  double* Tf = c->Tl.as<double>();
+  CK(launch_flip_transpose(S, lds, Sf, ldf, m, st));
+  CK(launch_flip_transpose(T, ldt, Tf, ldf, m, st));
+  std::vector<int> self;
+  if (select) {
+    self.resize(m);
+    for (int j = 0; j < m; ++j) self[m - 1 - j] = select[j];
+  }
+  int r = tgevc_device(c, m, Sf, ldf, Tf, ldf, select ? self.data() : nullptr, c->Xb.as<double>(), ldf,
+                       c->El.as<int>());
+  if (r > 0) return m - r;          // the 2x2 block at rows (r-1, r) of S' is rows (m-r-1, m-r) of S
+  if (r) return r;
+  const int n_sel = c->info.n_sel;
+  CK(launch_left_gather(c->Xb.as<double>(), ldf, Y, ldy, m, n_sel, c->coli.as<int>(), c->El.as<int>(), cse, st));
+  CK(cudaStreamSynchronize(st));
+  c->info.total_launches += 3;
+  return 0;
+}
+
 int check_args(int m, const double* S, int lds, const double* T, int ldt, double* X, int ldx) {
   if (m < 0) return -1;
   if (m > 0 && !S) return -2;
@@ -769,6 +807,19 @@ int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, con
     return 0;
   }
   return tgevc_back_device(g_ctx, m, S, lds, T, ldt, select, V, ldv, W, ldw, col_scale_exp);
+}
+
+int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* Y,
+                  int ldy, int* col_scale_exp) {
+  int a = check_args(m, S, lds, T, ldt, Y, ldy);
+  if (a) return a;
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (cudaSetDevice(g_ctx->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (m == 0) {
+    memset(&g_ctx->info, 0, sizeof(g_ctx->info));
+    return 0;
+  }
+  return tgevc_left_device(g_ctx, m, S, lds, T, ldt, select, Y, ldy, col_scale_exp);
 }
 
 int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 namespace zz {
 
 // ------------------------------------------------------------------------------------
@@ -185,5 +187,9 @@ cudaError_t launch_pack(const double* S, long long lds, const double* T, long lo
 int update_box_rows();   // rows per TMA box of the S/T tensor maps
 // zz_back.cu: LAPACK normalisation of the back-transformed columns (xTGEVC HOWMNY='B')
 cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const int* col_kind, cudaStream_t st);
+// zz_left.cu: left eigenvectors through the flipped pencil S' = J S^T J, T' = J T^T J
+cudaError_t launch_flip_transpose(const double* A, long long lda, double* B, long long ldb, int m, cudaStream_t st);
+cudaError_t launch_left_gather(const double* Xf, long long ldxf, double* Y, long long ldy, int m, int n_sel,
+                               const int* kind_f, const int* ef, int* ey, cudaStream_t st);
 
 }  // namespace zz

@@ -63,3 +63,29 @@ def dtgevc_back(S, T, V):
               T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), 1, VR.ctypes.data_as(vp), m, m,
               ctypes.byref(mo))
     return info, VR[:, :mo.value]
+
+
+def dtgevc_left(S, T, select=None):
+    """Left eigenvectors (SIDE='L', HOWMNY='A' or 'S'); returns (info, VL)."""
+    global _f
+    if _f is None:
+        lib = ctypes.CDLL(_paths()[0])
+        _f = lib.scipy_LAPACKE_dtgevc
+        _f.restype = ctypes.c_int
+    S = np.asfortranarray(S, dtype=np.float64)
+    T = np.asfortranarray(T, dtype=np.float64)
+    m = S.shape[0]
+    VL = np.zeros((m, max(m, 1)), order="F")
+    VR = np.zeros((1, 1))
+    mo = ctypes.c_int(0)
+    if select is None:
+        how, sel = b"A", None
+    else:
+        how = b"S"
+        sel = np.ascontiguousarray(np.asarray(select, dtype=np.int32))
+    vp = ctypes.c_void_p
+    info = _f(102, ctypes.c_char(b"L"), ctypes.c_char(how),
+              None if sel is None else sel.ctypes.data_as(vp), m, S.ctypes.data_as(vp), m,
+              T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), m, VR.ctypes.data_as(vp), 1, m,
+              ctypes.byref(mo))
+    return info, VL[:, :mo.value]

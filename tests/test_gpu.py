@@ -460,3 +460,58 @@ def test_back_select_ldw_and_residual(zz):
     ref = oracle.tgevc(S, T)
     D, Bm, _ = checks.build_DB(ref["pairs"], S)
     assert checks.residual(Q @ S @ V.T, Q @ T @ V.T, W0, D, Bm) <= 10 * m * 2.0 ** -53
+
+
+# ---- left eigenvectors (xTGEVC SIDE='L', include/zz.h zz_tgevc_left) ----
+
+def _left(zz, S, T, mb=0, select=None, ldy=None):
+    zz.set_tile(mb)
+    m = S.shape[0]
+    n = oracle.count_columns(S, select)
+    Y = None
+    if ldy is not None:
+        Y = torch.full((max(n, 1), ldy), np.nan, dtype=torch.float64, device="cuda").t()[:m, :n]
+    Y, e = zz.tgevc_left(to_dev(S), to_dev(T), select=select, Y=Y, n_sel=n)
+    torch.cuda.synchronize()
+    return Y.cpu().numpy(), e.cpu().numpy(), zz.last_info()
+
+
+@pytest.mark.parametrize("name,seed,mb", [("C1", 0, 32), ("C1", 3, 64), ("C2", 0, 128), ("C2", 2, 64)])
+def test_left_parity(zz, name, seed, mb):
+    S, T, _ = gen.config(name, seed=seed)
+    Y, e, info = _left(zz, S, T, mb=mb)
+    ref = oracle.tgevc_left(S, T)
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(Y, ref["Y"], lay)
+    assert np.isfinite(Y).all() and (e <= 0).all()
+    assert ali.max() <= TOL and raw.max() <= TOL, (ali.max(), raw.max())
+    for col, j, sz in lay:
+        assert np.all(Y[:j, col:col + sz] == 0.0)
+        if sz == 2:
+            assert e[col] == e[col + 1]
+
+
+def test_left_select_ldy_and_errors(zz):
+    S, T, _ = gen.config("C2", seed=1, m=700, n2=105)
+    m = S.shape[0]
+    Y0, e0, _ = _left(zz, S, T, mb=64)
+    Y1, e1, _ = _left(zz, S, T, mb=64, ldy=701)
+    assert np.array_equal(Y0, Y1) and np.array_equal(e0, e1)
+    sel = np.zeros(m, np.int32)
+    sel[3::11] = 1
+    Ys, es, _ = _left(zz, S, T, mb=64, select=sel)
+    lay_f = checks.column_layout(None, None, S)
+    lay_s = checks.column_layout(None, None, S, sel)
+    start = {j: col for col, j, _ in lay_f}
+    for col, j, sz in lay_s:
+        assert np.array_equal(Ys[:, col:col + sz], Y0[:, start[j]:start[j] + sz])
+    # status codes refer to S: a 2x2 block with real eigenvalues at rows 2-3 (1-based) -> +2
+    S2 = np.array([[0.5, 0.1, 0.2, 0.1], [0.0, 1.0, 0.3, 0.2], [0.0, 1.0, 1.0, 0.3], [0, 0, 0, 2.0]], order="F")
+    with pytest.raises(zz.ZZError) as ei:
+        _left(zz, S2, np.eye(4, order="F"), mb=32)
+    assert ei.value.status == 2 == oracle.tgevc_left(S2, np.eye(4, order="F"))["status"]
+    S3 = S2.copy()
+    S3[3, 2] = 1.0
+    with pytest.raises(zz.ZZError) as ei:
+        _left(zz, S3, np.eye(4, order="F"), mb=32)
+    assert ei.value.status == -105

@@ -363,3 +363,61 @@ def test_back_selected_subset_matches_full_columns():
     start = {j: col for col, j, _ in lay_f}
     for col, j, sz in lay_s:
         assert np.array_equal(sub["W"][:, col:col + sz], full["W"][:, start[j]:start[j] + sz])
+
+
+# ---- left eigenvectors (LAPACK xTGEVC SIDE='L'; include/zz.h zz_tgevc_left) ----
+
+def _left_residual(S, T, Y, lay, pairs):
+    """max over columns of ||y^H (beta S - alpha T)|| / ((|beta| ||S|| + |alpha| ||T||) ||y||)"""
+    worst = 0.0
+    nS, nT = np.linalg.norm(S), np.linalg.norm(T)
+    for col, j, sz in lay:
+        y = Y[:, col] + (1j * Y[:, col + 1] if sz == 2 else 0.0)
+        a, b, be = pairs[j]
+        al = a + 1j * abs(b)
+        r = np.conj(y) @ (be * S - al * T)
+        worst = max(worst, np.linalg.norm(r) / ((abs(be) * nS + abs(al) * nT) * np.linalg.norm(y)))
+    return worst
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_lapack_dtgevc_left_C1(seed):
+    _lapack_or_skip()
+    S, T, _ = gen.config("C1", seed=seed)
+    r = oracle.tgevc_left(S, T)
+    info, VL = lapack_pin.dtgevc_left(S, T)
+    assert info == 0 and r["status"] == 0
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(r["Y"], VL, lay)
+    assert ali.max() < 1e-11 and raw.max() < 1e-11, (ali.max(), raw.max())
+
+
+def test_lapack_left_larger_zero_inf_and_subset():
+    _lapack_or_skip()
+    S, T, _ = gen.generate(500, 75, 1.0 / 500, seed=7, gap_mode=2, gap=1e-4, n_zero=5, n_inf=5)
+    r = oracle.tgevc_left(S, T)
+    info, VL = lapack_pin.dtgevc_left(S, T)
+    lay = checks.column_layout(None, None, S)
+    raw, ali = checks.parity(r["Y"], VL, lay)
+    assert info == 0 and ali.max() < 1e-10, ali.max()
+    sel = np.zeros(500, np.int32)
+    sel[[0, 3, 100, 101, 250, 499]] = 1
+    rs = oracle.tgevc_left(S, T, select=sel)
+    info, VLs = lapack_pin.dtgevc_left(S, T, select=sel)
+    lay_s = checks.column_layout(None, None, S, sel)
+    raw, ali = checks.parity(rs["Y"], VLs, lay_s)
+    assert info == 0 and ali.max() < 1e-10, ali.max()
+
+
+def test_left_definition_zeros_and_status():
+    S, T, _ = gen.config("C1", seed=6)
+    r = oracle.tgevc_left(S, T)
+    a, b, be, kd, st = oracle.eig_pairs(S, T)
+    pairs = np.stack([a, b, be], axis=1)
+    lay = checks.column_layout(None, None, S)
+    assert _left_residual(S, T, r["Y"], lay, pairs) < 1e-14
+    for col, j, sz in lay:     # exact zeros above the eigenvalue's block
+        assert np.all(r["Y"][:j, col:col + sz] == 0.0)
+    # a 2x2 block with real eigenvalues is reported by its first row in S (1-based)
+    S2 = np.array([[0.5, 0.1, 0.2, 0.1], [0.0, 1.0, 0.3, 0.2], [0.0, 1.0, 1.0, 0.3], [0, 0, 0, 2.0]], order="F")
+    assert oracle.tgevc_left(S2, np.eye(4, order="F"))["status"] == 2 == oracle.tgevc(S2, np.eye(4, order="F"))["status"]
