@@ -30,6 +30,7 @@ import gen  # noqa: E402
 
 METRIC = "seconds & FP64 TFLOP/s, all eigenvectors, m=40000, at 1/2/4/8 B200"
 STAGED_BYTES = None
+D2H_BYTES = None
 FP64_PEAK = 37.0   # TFLOP/s, measured DMMA.8x8x4 loop on this pool (profiles/r01_fp64_peak.json)
 PEAK_SRC = ("measured: DMMA.8x8x4 / DFMA register loops 37.0 / 37.1 TFLOP/s at 1965 MHz, cuBLAS "
             "DGEMM 35.5 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry "
@@ -76,8 +77,12 @@ def update_flops(blocks, m, mb):
         last[j:j + sz] = j + sz - 1
     tile_of_row = np.repeat(np.arange(M), np.diff(ts))
     # bytes zz_tgevc_host stages per matrix: each tile column's rows up to the subdiagonal
-    global STAGED_BYTES
+    global STAGED_BYTES, D2H_BYTES
     STAGED_BYTES = float(sum(min(ts[I + 1] + 1, m) * (ts[I + 1] - ts[I]) for I in range(M))) * 8.0
+    # zz_tgevc_host downloads rows 0 .. max r_c of each 64-column block (all columns: column c
+    # of block order = row c; the zeros below are written on the host) + the exponents
+    D2H_BYTES = float(sum((int(last[min(c0 + 63, m - 1)]) + 1) * min(64, m - c0) for c0 in range(0, m, 64))) * 8.0 \
+        + 4.0 * m
     tcol = tile_of_row[last]
     per = []
     for I in range(M - 1, 0, -1):
@@ -347,9 +352,11 @@ def main():
             zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
         te = (time.perf_counter() - t0) / ks
         res["e2e"] = {"value": F / te * 1e-12, "unit": "TFLOP/s", "seconds_per_step": te,
-                      "h2d_bytes_per_step": int(2 * STAGED_BYTES), "d2h_bytes_per_step": m * m * 8 + m * 4,
+                      "h2d_bytes_per_step": int(2 * STAGED_BYTES), "d2h_bytes_per_step": int(D2H_BYTES),
                       "steps": ks, "api": "zz_tgevc_host (pinned host S, T, X; S and T staged by tile "
-                                          "column in consumption order, upper part only, overlapped)"}
+                                          "column in consumption order, upper part only, overlapped; "
+                                          "X downloaded upper part only, zeros written by host threads "
+                                          "during the solve)"}
         Xd_check = Xd
     if rank == 0 and world == 1 and not args.no_cpu:
         Sn, Tn = Sh.numpy(), Th.numpy()

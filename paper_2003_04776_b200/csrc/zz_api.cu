@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "../../include/zz.h"
@@ -845,11 +846,43 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
   CK(cudaStreamWaitEvent(c->copy, c->e_copy, 0));
   HostStage hs;
   hs.Sh = S; hs.ldsh = lds; hs.Th = T; hs.ldth = ldt; hs.copy = c->copy; hs.ev = &c->ev_copy;
+  // X is block-upper-triangular: column c is zero below its last row r_c.  Only the upper
+  // part travels back over PCIe (one 2D copy per 64-column block, rows 0 .. the block's
+  // largest r_c); the zeros below are written by host threads while the GPU solves (the
+  // regions are disjoint, and the device never touches X before the download).
+  std::vector<int> rmax;   // per 64-column block
+  {
+    int col = 0, j = 0;
+    rmax.assign((size_t)(n_sel + 63) / 64, -1);
+    while (j < m) {
+      const bool two = j + 1 < m && S[(size_t)j * lds + j + 1] != 0.0;
+      const int sz = two ? 2 : 1;
+      if (!select || select[j] || (two && select[j + 1]))
+        for (int q = 0; q < sz; ++q, ++col) rmax[col / 64] = j + sz - 1;
+      j += sz;
+    }
+  }
+  const int nthr = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+  std::vector<std::thread> zt;
+  for (int w = 0; w < nthr && n_sel > 0; ++w)
+    zt.emplace_back([=, &rmax]() {
+      for (int cb = w; cb < (int)rmax.size(); cb += nthr) {
+        const int r0 = rmax[cb] + 1;
+        if (r0 >= m) continue;
+        for (int cc = cb * 64; cc < std::min(n_sel, cb * 64 + 64); ++cc)
+          memset(X + (size_t)cc * ldx + r0, 0, sizeof(double) * (size_t)(m - r0));
+      }
+    });
   int r = tgevc_device(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
                        c->hE.as<int>(), &hs);
+  for (auto& th : zt) th.join();
   if (r) return r;
   if (n_sel > 0) {
-    CK(cudaMemcpy2DAsync(X, (size_t)ldx * 8, c->hX.p, ld * 8, (size_t)m * 8, n_sel, cudaMemcpyDeviceToHost, st));
+    for (int cb = 0; cb < (int)rmax.size(); ++cb) {
+      const int c0 = cb * 64, nc = std::min(64, n_sel - c0);
+      CK(cudaMemcpy2DAsync(X + (size_t)c0 * ldx, (size_t)ldx * 8, c->hX.as<double>() + (size_t)c0 * ld, ld * 8,
+                           (size_t)(rmax[cb] + 1) * 8, nc, cudaMemcpyDeviceToHost, st));
+    }
     if (col_scale_exp)
       CK(cudaMemcpyAsync(col_scale_exp, c->hE.p, sizeof(int) * n_sel, cudaMemcpyDeviceToHost, st));
   }
