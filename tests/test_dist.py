@@ -34,8 +34,10 @@ def _worker(rank, world, port, name, seed, nb, q):
         S = torch.from_numpy(np.ascontiguousarray(S0.T)).t()
         T = torch.from_numpy(np.ascontiguousarray(T0.T)).t()
     else:
-        S = torch.zeros((m, m), dtype=torch.float64).t()
-        T = torch.zeros((m, m), dtype=torch.float64).t()
+        # NaN everywhere: the broadcast must deliver every entry the solve reads (the
+        # upper part and the subdiagonal) and nothing below is read
+        S = torch.full((m, m), float("nan"), dtype=torch.float64).t()
+        T = torch.full((m, m), float("nan"), dtype=torch.float64).t()
 
     def compute(S_, T_, sel):
         r = oracle.tgevc(S_.numpy(), T_.numpy(), select=sel)
@@ -48,12 +50,12 @@ def _worker(rank, world, port, name, seed, nb, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("nb", [8, 32])
-def test_two_rank_sharding_bitwise(nb):
+@pytest.mark.parametrize("nb,world", [(8, 2), (32, 2), (8, 3)])
+def test_two_rank_sharding_bitwise(nb, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, "C1", 3, nb, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "C1", 3, nb, q)) for r in range(world)]
     for p in procs:
         p.start()
     X, E = q.get(timeout=120)
@@ -64,6 +66,13 @@ def test_two_rank_sharding_bitwise(nb):
     ref = oracle.tgevc(S0, T0)
     assert np.array_equal(X, ref["X"])
     assert np.array_equal(E, ref["e"])
+
+
+def test_upper_chunks_cover_the_columns():
+    for m in (1, 2, 7, 96, 1000):
+        ch = zdist.upper_chunks(m)
+        assert ch[0][0] == 0 and ch[-1][1] == m
+        assert all(a < b for a, b in ch) and all(ch[i][1] == ch[i + 1][0] for i in range(len(ch) - 1))
 
 
 def test_shard_select_partitions_columns():

@@ -515,3 +515,17 @@ def test_left_select_ldy_and_errors(zz):
     with pytest.raises(zz.ZZError) as ei:
         _left(zz, S3, np.eye(4, order="F"), mb=32)
     assert ei.value.status == -105
+
+
+def test_lower_parts_never_read(zz):
+    # the contract the multi-GPU broadcast relies on (dist.broadcast_upper sends only the
+    # upper trapezoid): NaN below the subdiagonal of S and below the diagonal of T changes
+    # nothing, bit for bit
+    S, T, _ = gen.config("C2", seed=0, m=600, n2=90)
+    X0, e0, _ = solve(zz, S, T, mb=64)
+    Sn, Tn = S.copy(order="F"), T.copy(order="F")
+    il = np.tril_indices(600, -2)
+    Sn[il] = np.nan
+    Tn[np.tril_indices(600, -1)] = np.nan
+    X1, e1, _ = solve(zz, Sn, Tn, mb=64)
+    assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
