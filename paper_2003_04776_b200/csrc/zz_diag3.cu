@@ -306,6 +306,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     }
     __syncwarp();
     int j = e0 - 1;
+    int kseg = 0;
     while (j >= s0) {
       const int q = j - (g8 - 1);
       const bool two = sm.fl[j] == kRowBot2;
@@ -388,9 +389,11 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         bound = nb;
       }
       if (k + eu < 0) {
-        // the whole segment by 2^(k+eu): pending rows in registers, the block's rows in the slab
+        // the whole segment by 2^(k+eu): the block's rows in the slab now, the rows in
+        // registers once after the row loop (kseg) -- s.y is then not modified inside the
+        // loop, so it keeps its registers (no copies around the loop; powers of two)
         const int kk = k + eu;
-        s.scale(kk);
+        kseg += kk;
         // slot r of the slab is always written by lane r & 3 of its column (here and in the
         // update below), so no warp barrier is needed in this column-divergent branch
         for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], kk);
@@ -427,6 +430,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       j = qs - 1 + (g8 - 1);
     }
     // ---- the block's rows back to their owner lanes ----
+    if (kseg < 0) s.scale(kseg);
     s.y[CUR][0] = wslab[(1 + 2 * t) * 8 + team];
     s.y[CUR][1] = wslab[(2 + 2 * t) * 8 + team];
     if (st && t == 3) s.y[PRV][1] = wslab[team];
