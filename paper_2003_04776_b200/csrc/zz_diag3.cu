@@ -636,25 +636,26 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // ---- stage the diagonal tile: (S_ij, T_ij) for i <= j, (S_{j+1,j}, 0) below ----
   const int plen = nt * (nt + 3) / 2;
+  // asynchronous 8-byte global->shared copies (cp.async): every element of the tile is in
+  // flight at once instead of one column per warp at a time (the staging was a third of the
+  // kernel's time on latency-bound steps)
   for (int j = warp; j < nt; j += kW3) {
     const int len = min(j + 2, nt);
     const double* sc = p.S + (long long)(p.t0 + j) * p.lds + p.t0;
     const double* tc = p.T + (long long)(p.t0 + j) * p.ldt + p.t0;
-    double sv[5], tv[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int i = lane + 32 * q;
-      sv[q] = (i < len) ? sc[i] : 0.0;
-      tv[q] = (i < len && i <= j) ? tc[i] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int i = lane + 32 * q;
-      if (i < len) sm.ST[poff3(j) + i] = make_double2(sv[q], tv[q]);
+    double2* col = sm.ST + poff3(j);
+    for (int i = lane; i < len; i += 32) {
+      const unsigned ds = (unsigned)__cvta_generic_to_shared(&col[i]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(ds), "l"(sc + i) : "memory");
+      if (i <= j)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(ds + 8u), "l"(tc + i) : "memory");
+      else
+        col[i].y = 0.0;
     }
   }
   for (int i = threadIdx.x; i < kPad3; i += blockDim.x) sm.ST[plen + i] = make_double2(0.0, 0.0);
   for (int i = threadIdx.x; i < nt; i += blockDim.x) sm.fl[i] = p.P.row_flag[p.t0 + i];
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int nblk = (nt + 7) / 8;
   if (threadIdx.x <= nblk) {
@@ -668,6 +669,7 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   for (int j = threadIdx.x; j < nt; j += blockDim.x) {
     const int top = (sm.fl[j] == kRowBot2) ? j - 1 : j;
     double ms = 0.0, mt = 0.0;
+#pragma unroll 8
     for (int i = 0; i < top; ++i) {
       const double2 v = sm.ST[poff3(j) + i];
       ms = fmax(ms, fabs(v.x));

@@ -182,7 +182,7 @@ __global__ void k_panel_norms(const double* __restrict__ S, long long lds,
     const double* sp = S + (long long)i;
     const double* tp = T + (long long)i;
     int k = kb;
-#pragma unroll 4
+#pragma unroll 16
     for (; k < k1; ++k) {
       s += fabs(sp[(long long)k * lds]);
       t += fabs(tp[(long long)k * ldt]);
@@ -212,6 +212,8 @@ __global__ void k_diag0_norms(const double* __restrict__ S, long long lds,
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0, t = 0.0;
   if (i < k1) {
+    // unrolled: the loads of 16 columns are in flight together (the sums keep their order)
+#pragma unroll 16
     for (int k = max(0, i - 1); k < k1; ++k) {
       s += fabs(S[(long long)k * lds + i]);
       t += fabs(T[(long long)k * ldt + i]);
