@@ -86,6 +86,13 @@ int zz_set_tile(int mb);
  * zz_info_t.ms_update.  Adds an event pair per step; used by bench.py for the roofline. */
 int zz_set_timing(int on);
 
+/* Step grouping of the wavefront for this thread's context: 1 = one update launch per step;
+ * 2 = pairs of steps share one update of the rows above them with K = 2 tiles;
+ * 3 (default) = triples (K = 3 tiles).  Results differ only by summation order (DESIGN.md s.6);
+ * groups are fixed by the tile index, so results never depend on `select`.  Tiles of more
+ * than 128 rows always run ungrouped.  Returns 0, -1 (k not in 1..3) or -103. */
+int zz_set_fusion(int k);
+
 /*
  * zz_tgevc: selected right eigenvectors on the device.
  *   m              order of S and T (m >= 0)                                   [arg 1]

@@ -27,7 +27,7 @@ STATUS = {
     -106: "unsupported tile size",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -78,6 +78,7 @@ def load(build_if_missing=True):
         "zz_set_stream": ([vp], ci),
         "zz_set_tile": ([ci], ci),
         "zz_set_timing": ([ci], ci),
+        "zz_set_fusion": ([ci], ci),
         "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_back": ([ci, vp, ci, vp, ci, vp, vp, ci, vp, ci, vp], ci),
@@ -117,6 +118,11 @@ def init(device=None):
 
 def set_tile(mb):
     _check(load().zz_set_tile(int(mb)), "zz_set_tile")
+
+
+def set_fusion(k):
+    """Step grouping of the wavefront: 1, 2 or 3 (default) consecutive steps per update."""
+    _check(load().zz_set_fusion(int(k)), "zz_set_fusion")
 
 
 def set_timing(on):

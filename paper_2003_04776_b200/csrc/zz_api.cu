@@ -58,10 +58,12 @@ struct Context {
   cudaStream_t stream = nullptr;
   int mb = 0;
   int timing = 0;
+  // step groups of the wavefront: 1 (none), 2 (pairs) or 3 (triples); zz_set_fusion, ZZ_FUSE
+  int fusion = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 3;
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
-  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, status, tmp, Sc, Tc, Apk, Xi;
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, W3, status, tmp, Sc, Tc, Apk, Xi;
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
   Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
@@ -75,7 +77,7 @@ struct Context {
   ~Context() {}
   void release() {
     Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W, &W2,
-                  &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
+                  &W3, &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     Xb.release();
     Sl.release();
@@ -277,7 +279,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
   CK(c->rows.ensure((sizeof(int) + 1) * (size_t)m + 16));
   CK(c->blks.ensure(sizeof(int) * 3 * (size_t)nb));
-  CK(c->state.ensure(sizeof(unsigned long long) * 2 * (size_t)n));
+  CK(c->state.ensure(sizeof(unsigned long long) * 3 * (size_t)n));
   CK(c->seg.ensure((sizeof(int) + 2 * sizeof(double)) * (size_t)M * n));
   CK(c->norms.ensure(sizeof(double) * 4 * (size_t)M));
   CK(c->W.ensure(sizeof(double) * (size_t)n_ntiles_all * 2 * nks_max * kBN * kBK));
@@ -436,7 +438,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     if (r) return r;
   }
   CK(cudaMemsetAsync(P.e_pend, 0, sizeof(int) * n, st));
-  CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * 2 * n, st));
+  CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * 3 * n, st));
   CK(cudaEventRecord(c->e1, st));
   // ---- the wavefront (Algorithm 1 over tile rows, bottom-up) ----
   // X with an odd leading dimension or a base that is not 16-byte aligned: solve into an
@@ -464,9 +466,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   // 128-row band), tile J is solved, and the rows above tile J get both steps' updates in one
   // contraction with K = [tile J | tile I] (twice the K of a single step: half the C-tile
   // traffic and prologue/epilogue per flop).
-  static const int fuse_env = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 1;
-  const bool can_fuse = fuse_env && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
+  const int fusion = std::max(1, std::min(3, c->fusion));
+  const bool can_fuse = fusion > 1 && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
   CK(c->W2.ensure(c->W.cap));
+  if (fusion == 3) CK(c->W3.ensure(c->W.cap));
   int nyb = (M - 1) & 1;   // nY buffer holding the pending max for the next decision
   static const bool dbg_sync = getenv("ZZ_DEBUG_SYNC") != nullptr;
   auto dbg = [&](const char* what, int I) -> int {
@@ -520,19 +523,28 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.nY_in = dp.nY_in;
       d2.Wout = Wout;
       if (fuse_from) {
-        d2.fused = 1;
-        d2.Iprev = fuse_from->I;
-        d2.cs_prev = cs[fuse_from->I];
-        d2.zero_pend_end = cs[fuse_from->I + 1];
-        d2.Wprev = fuse_from->Wout;
-        d2.nks_prev = fuse_from->nks;
+        // step-group role (zz_diag3.cu): fused = 1 last step of a pair, 2 middle step of a
+        // triple (band decision, nY buffer 2), 3 last step of a triple; reset_band: first
+        // step of a triple
+        d2.fused = fuse_from->fused;
+        d2.Iprev = fuse_from->Iprev;
+        d2.cs_prev = fuse_from->cs_prev;
+        d2.zero_pend_end = fuse_from->zero_pend_end;
+        d2.Wprev = fuse_from->Wprev;
+        d2.nks_prev = fuse_from->nks_prev;
+        d2.Jprev = fuse_from->Jprev;
+        d2.cs_prev2 = fuse_from->cs_prev2;
+        d2.Wprev2 = fuse_from->Wprev2;
+        d2.nks_prev2 = fuse_from->nks_prev2;
+        d2.reset_band = fuse_from->reset_band;
+        if (d2.fused == 2) d2.nY_in = 2;
       }
       CK(launch_diag3(d2, st));
     } else {
       CK(launch_diag(dp, st));
     }
     launches++;
-    return dbg(fuse_from ? "diag (fused)" : "diag", I);
+    return dbg(fuse_from && fuse_from->fused ? "diag (fused)" : "diag", I);
   };
   auto update = [&](UpdParams up, int n_m) -> int {
     const int n_n = ceil_div(n_sel, kBN) - up.ntile0;
@@ -567,27 +579,87 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     int r = panel_ready(I);
     if (r) return r;
     if (tile_item[I] >= n_items) { --I; continue; }
-    const int J = I - 1;
-    // pairs are fixed by the tile index alone ((M-1-I) even), not by which steps have active
-    // columns, so a column's operations do not depend on the selection (sharding, select)
-    if (can_fuse && J >= 1 && ((M - 1 - I) & 1) == 0) {
+    // Step groups are fixed by the tile index alone (groups of `fusion` consecutive steps
+    // counted from M-1), not by which steps have active columns: a step that opens the
+    // solve in the middle of its group runs the group's remaining steps, so a column's
+    // operations do not depend on the selection (sharding, select).  The last step of a
+    // fused group needs rows above it (index >= 1).
+    int len = 1;
+    if (can_fuse) {
+      len = fusion - (M - 1 - I) % fusion;
+      while (len > 1 && I - (len - 1) < 1) --len;
+    }
+    const int J = I - 1, K = I - 2;
+    auto nks_of = [&](int t) { return ceil_div(ts[t + 1] - ts[t], kBK); };
+    if (len == 3) {
+      // ---- three-step group (I, J, K): thin updates of the band of tiles J, K; one update
+      // above tile K with K = [tile K | tile J | tile I] ----
+      Diag2Params oi;
+      memset(&oi, 0, sizeof(oi));
+      oi.reset_band = 1;
+      if ((r = diag(I, P.W, &oi))) return r;
+      UpdParams th = base_up(I);            // rows of tiles K and J; band max over tile K's rows
+      th.row_lo = ts[K];
+      th.max_row = ts[J];
+      th.nY_out = P.nY + 2 * (size_t)n;
+      if ((r = update(th, ceil_div(ts[I] - (ts[K] & ~1), kBM)))) return r;
+      if ((r = panel_ready(J))) return r;
+      Diag2Params oj;
+      memset(&oj, 0, sizeof(oj));
+      oj.fused = 2;
+      if ((r = diag(J, c->W2.as<double>(), &oj))) return r;
+      UpdParams tj = base_up(J);            // rows of tile K with W_J
+      tj.row_lo = ts[K];
+      tj.max_row = 0;
+      tj.W = c->W2.as<double>();
+      if ((r = update(tj, ceil_div(ts[J] - (ts[K] & ~1), kBM)))) return r;
+      if ((r = panel_ready(K))) return r;
+      Diag2Params ok;
+      memset(&ok, 0, sizeof(ok));
+      ok.fused = 3;
+      ok.Iprev = I;
+      ok.cs_prev = cs[I];
+      ok.Jprev = J;
+      ok.cs_prev2 = cs[J];
+      ok.zero_pend_end = cs[I + 1];
+      ok.Wprev = P.W;
+      ok.nks_prev = nks_of(I);
+      ok.Wprev2 = c->W2.as<double>();
+      ok.nks_prev2 = nks_of(J);
+      if ((r = diag(K, c->W3.as<double>(), &ok))) return r;
+      UpdParams fu = base_up(K);
+      fu.W = c->W3.as<double>();
+      fu.first_end = cs[I + 1];             // tips of I, J and K start from zero pending rows
+      fu.t0b = ts[J]; fu.nksb = nks_of(J); fu.Wb = c->W2.as<double>();
+      fu.t0c = ts[I]; fu.nksc = nks_of(I); fu.Wc = P.W;
+      if ((r = update(fu, ceil_div(ts[K], kBM)))) return r;
+      nyb = 1 - nyb;
+      ++n_fused;
+      I -= 3;
+      continue;
+    }
+    if (len == 2) {
       // ---- fused pair (I, J) ----
-      Diag2Params first;
-      first.I = I;
-      first.nks = ceil_div(ts[I + 1] - ts[I], kBK);
-      first.Wout = P.W;
       if ((r = diag(I, P.W, nullptr))) return r;
       UpdParams thin = base_up(I);          // rows of tile J only, no column maximum
       thin.row_lo = ts[J];
       thin.max_row = 0;
       if ((r = update(thin, ceil_div(ts[I] - (ts[J] & ~1), kBM)))) return r;
       if ((r = panel_ready(J))) return r;
-      if ((r = diag(J, c->W2.as<double>(), &first))) return r;
+      Diag2Params oj;
+      memset(&oj, 0, sizeof(oj));
+      oj.fused = 1;
+      oj.Iprev = I;
+      oj.cs_prev = cs[I];
+      oj.zero_pend_end = cs[I + 1];
+      oj.Wprev = P.W;
+      oj.nks_prev = nks_of(I);
+      if ((r = diag(J, c->W2.as<double>(), &oj))) return r;
       UpdParams fu = base_up(J);            // rows above tile J, K = [tile J | tile I]
       fu.W = c->W2.as<double>();
       fu.first_end = cs[I + 1];             // tips of I and J start from zero pending rows
       fu.t0b = ts[I];
-      fu.nksb = first.nks;
+      fu.nksb = nks_of(I);
       fu.Wb = P.W;
       if ((r = update(fu, ceil_div(ts[J], kBM)))) return r;
       nyb = 1 - nyb;
@@ -772,6 +844,13 @@ int zz_set_tile(int mb) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (mb != 0 && (mb < 32 || mb > kMaxMB || (mb % 16) != 0)) return ZZ_ERR_TILE;
   g_ctx->mb = mb;
+  return 0;
+}
+
+int zz_set_fusion(int k) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (k < 1 || k > 3) return -1;
+  g_ctx->fusion = k;
   return 0;
 }
 

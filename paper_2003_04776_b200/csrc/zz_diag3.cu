@@ -522,7 +522,68 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       P.nrm_seg[so] = lm;
       P.nrmh_seg[so] = lh;
     }
-    if (p.do_update && p.fused) {
+    if (p.do_update && p.fused == 3) {
+      // last step K of a three-step group (I, J = I - 1, K = I - 2): one update of the rows
+      // above tile K (region R, still at the exponent e_p of before step I) with all three
+      // tiles, K = [tile K | tile J | tile I].  W_I is at e1 (step I's decision), W_J at
+      // e2 = e_pend (step J's band decision, reading R5 on tile K's rows), W_K at es.  The
+      // decision bounds all four terms as the two-step one does:
+      //   2^(ef-e_p) y^_R + sum_X tau_X 2^(ef-e_X) x^_X <= 2^(ef-g)(y^ + (sum tau) max_X x^_X 2^(g-e_X)) <= Omega
+      const bool act_i = c0 >= p.cs_prev;                     // active at step I
+      const bool act_j = c0 >= p.cs_prev2;                    // active at step J
+      const int e2 = ep;
+      const int e_p = act_i ? P.e_prev[c] : 0;                // written by step I only
+      const int e1 = act_i ? e2 - P.sY[c] : 0;                // step J's shift of the band: e2 - e1
+      const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
+      double nyv = 0.0;
+      if (c0 >= p.zero_pend_end) {                            // not a tip of I, J or K
+        nyv = __longlong_as_double((long long)nyi[c0]);
+        if (PAIR) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
+      }
+      const int g0 = min(e2, es);
+      double xh = scale2k(lm, g0 - es);
+      double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
+      if (act_j) {
+        const long long sp = (long long)p.Jprev * p.n_sel + c;
+        xh = dmaxd(xh, scale2k(P.nrm_seg[sp], g0 - P.e_seg[sp]));
+        tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Jprev]), __dmul_rn(ab, P.cT[p.Jprev])));
+      }
+      if (act_i) {
+        const long long sp = (long long)p.Iprev * p.n_sel + c;
+        xh = dmaxd(xh, scale2k(P.nrm_seg[sp], g0 - P.e_seg[sp]));
+        tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Iprev]), __dmul_rn(ab, P.cT[p.Iprev])));
+      }
+      const double yh = scale2k(nyv, g0 - e_p);
+      const int ef = g0 + protect_update(yh, tau, xh);
+      sx = ef - es;
+      if (t == 0) {
+        P.sY[c] = ef - e_p;
+        P.e_pend[c] = ef;
+        P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
+      }
+      // W_I and W_J of this column brought to ef (rare), or zero where the column was not
+      // active at that step (stale entries)
+      if (!act_i || ef != e1) {
+        const long long tstr = (long long)(2 * p.nks_prev) * (kBN * kBK);
+        const long long hf = (long long)p.nks_prev * (kBN * kBK);
+        double* Wp = p.Wprev + (long long)(c / kBN) * tstr + (c % kBN) * 4;
+        for (int r = t; r < p.nks_prev * kBK; r += 4) {
+          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
+          Wp[off] = act_i ? scale2k(Wp[off], ef - e1) : 0.0;
+          Wp[off + hf] = act_i ? scale2k(Wp[off + hf], ef - e1) : 0.0;
+        }
+      }
+      if (!act_j || ef != e2) {
+        const long long tstr = (long long)(2 * p.nks_prev2) * (kBN * kBK);
+        const long long hf = (long long)p.nks_prev2 * (kBN * kBK);
+        double* Wp = p.Wprev2 + (long long)(c / kBN) * tstr + (c % kBN) * 4;
+        for (int r = t; r < p.nks_prev2 * kBK; r += 4) {
+          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
+          Wp[off] = act_j ? scale2k(Wp[off], ef - e2) : 0.0;
+          Wp[off + hf] = act_j ? scale2k(Wp[off + hf], ef - e2) : 0.0;
+        }
+      }
+    } else if (p.do_update && p.fused == 1) {
       // second step J of a fused pair (I, J = I - 1): one update of the rows above tile J with
       // both tiles (K = [tile J | tile I]).  Those rows are still at the exponent e_p they had
       // before step I (step I only updated tile J's rows, the thin update); step I's W_I is at
@@ -573,6 +634,9 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     } else if (p.do_update) {
       // Alg. 3 with Alg. 2, reading R5; pending max of the column
       // (pairs: of both columns)
+      // (fused == 2: the middle step J of a three-step group -- the decision covers tile K's
+      // rows only, whose maximum the thin update of step I left in buffer nY_in = 2; the
+      // exponent e_p of the rows above tile K stays in e_prev for step K)
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
       double nyv = tip ? 0.0 : __longlong_as_double((long long)nyi[c0]);
       if (PAIR && !tip) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
@@ -583,9 +647,10 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       sx = en - es;
       if (t == 0) {
         P.sY[c] = en - ep;
-        P.e_prev[c] = ep;       // the pending exponent before this step (read by a fused J)
+        if (p.fused != 2) P.e_prev[c] = ep;   // the pending exponent before this step (read by a fused J/K)
         P.e_pend[c] = en;
-        P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
+        if (p.fused != 2) P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
+        if (p.reset_band) P.nY[2LL * p.n_sel + c] = 0ull;   // the band maximum of a three-step group
       }
     }
   }

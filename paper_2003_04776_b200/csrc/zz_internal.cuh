@@ -78,7 +78,7 @@ struct DevPlan {
   int* e_pend;        // per column: exponent of the pending (not yet solved) rows
   int* sY;            // per column: exponent shift of the pending rows at this step
   int* e_prev;        // per column: pending exponent before the last decision (fused pairs)
-  unsigned long long* nY;   // 2 x n_sel: max |pending| (double bits), double buffered
+  unsigned long long* nY;   // 3 x n_sel: max |pending| (double bits), double buffered + band
   int* e_seg;         // M x n_sel: exponent of each solved segment
   double* nrm_seg;    // M x n_sel: max(|Re|,|Im|) of the segment
   double* nrmh_seg;   // M x n_sel: max(|x|/2 + |y|/2) (pair) or |x|/2 (real)
@@ -125,6 +125,9 @@ struct UpdParams {
   // per part) against Wb; nksb = 0 if absent
   int t0b, nksb;
   const double* Wb;
+  // optional third segment (three-step group): tile t0c, nksc chunks per part, Wc
+  int t0c, nksc;
+  const double* Wc;
   int l2hint;        // L2 eviction priorities: C evict_first, W evict_last (set by launch_update)
 };
 
@@ -155,6 +158,13 @@ struct Diag2Params {
   int zero_pend_end;       // columns < zero_pend_end (tips of I and J) have no pending rows
   double* Wprev;
   int nks_prev;
+  // three-step groups (I, J = I-1, K = I-2): fused = 2 marks step J (band decision on tile
+  // K's rows, nY_in = 2), fused = 3 step K (one update above tile K with all three tiles);
+  // Jprev/cs_prev2/Wprev2/nks_prev2 describe step J for step K; reset_band (step I) zeroes
+  // the band-maximum buffer nY[2]
+  int Jprev, cs_prev2, nks_prev2;
+  double* Wprev2;
+  int reset_band;
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)

@@ -325,13 +325,16 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // MODE 1 (two-step fused update): a second K segment; MODE 2 (thin update): first row row_lo
   constexpr bool SEG2 = MODE == 1;
-  const int nkca = 2 * p.nks, nkc = nkca + (SEG2 ? 2 * p.nksb : 0);   // K chunks: a, then b
+  // K chunks: segment a, then b, then c (MODE 1; a step group of two or three tiles)
+  const int nkca = 2 * p.nks, nkcb = SEG2 ? 2 * p.nksb : 0, nkcc = SEG2 ? 2 * p.nksc : 0;
+  const int nkc = nkca + nkcb + nkcc;
   const int n_ntl = n_tiles / n_mtiles;
   const int row_lo = (MODE == 2) ? p.row_lo : 0;
   const int mbase = row_lo & ~1;                         // 16-byte aligned first row pair
   // W is stored per 64-column block: [ntile64][kc][BK/4][64][4] (per segment)
   const long long wtile = (long long)nkca * (kBN * kBK);
   const long long wtileb = (long long)(2 * p.nksb) * (kBN * kBK);
+  const long long wtilec = (long long)(2 * p.nksc) * (kBN * kBK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -357,11 +360,11 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           const int s = g % kStages;
           if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
           mbar_expect_tx(&full[s], kABytes + nblk * kBBytes);
-          const bool sb = SEG2 && kc >= nkca;              // segment b
-          const int kl = sb ? kc - nkca : kc;              // chunk within its segment
-          const int nks_s = sb ? p.nksb : p.nks;
+          const int sg = !SEG2 ? 0 : (kc < nkca ? 0 : (kc < nkca + nkcb ? 1 : 2));   // segment
+          const int kl = kc - (sg == 0 ? 0 : (sg == 1 ? nkca : nkca + nkcb));   // chunk within it
+          const int nks_s = sg == 0 ? p.nks : (sg == 1 ? p.nksb : p.nksc);
           const CUtensorMap* tm = (kl < nks_s) ? &tmS : &tmT;
-          const int kcol = (sb ? p.t0b : p.t0) + (kl % nks_s) * kBK;
+          const int kcol = (sg == 0 ? p.t0 : (sg == 1 ? p.t0b : p.t0c)) + (kl % nks_s) * kBK;
           double* a = sA + s * (kBM * kBK);
           if (BOX == 0) {
             // packed panel (k_pack): one 16 KB bulk copy per stage
@@ -374,7 +377,9 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           }
           for (int q = 0; q < nblk; ++q)
             bulk_load_h(sB + s * (C::BN * kBK) + q * (kBN * kBK),
-                        (sb ? p.Wb + (long long)(nb64 + q) * wtileb : p.W + (long long)(nb64 + q) * wtile) +
+                        (sg == 0 ? p.W + (long long)(nb64 + q) * wtile
+                                 : (sg == 1 ? p.Wb + (long long)(nb64 + q) * wtileb
+                                            : p.Wc + (long long)(nb64 + q) * wtilec)) +
                             (long long)kl * (kBN * kBK),
                         kBBytes, &full[s], pol_w);
         }

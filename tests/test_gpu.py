@@ -189,12 +189,12 @@ def test_leading_dimensions_and_alignment(zz):
 
 
 def test_repeat_bitwise_fused_pairs(zz):
-    # full 128-row tiles: every fused update runs K = 2 x 256 (32 pipeline chunks); repeated
+    # full 128-row tiles: every grouped update runs K = 3 x 256 (48 pipeline chunks); repeated
     # solves and an odd ldx (internal aligned workspace) must give identical bits -- this is
-    # the regression test of the stage-release race of the update pipeline (DESIGN.md s.7)
+    # the regression test of the stage-release race of the update pipeline (DESIGN.md s.6)
     S, T, _ = gen.config("C3", seed=1, m=3000, n2=450)
     X0, e0, info = solve(zz, S, T, mb=128)
-    assert info["n_tiles"] >= 20 and info["fused_pairs"] >= 9
+    assert info["n_tiles"] >= 20 and info["fused_pairs"] >= 6
     for _ in range(3):
         X1, e1, _ = solve(zz, S, T, mb=128)
         assert np.array_equal(X1, X0) and np.array_equal(e1, e0)
@@ -529,3 +529,49 @@ def test_lower_parts_never_read(zz):
     Tn[np.tril_indices(600, -1)] = np.nan
     X1, e1, _ = solve(zz, Sn, Tn, mb=64)
     assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
+
+
+# ---- step grouping of the wavefront (zz_set_fusion 1 / 2 / 3) ----
+
+@pytest.mark.parametrize("fusion", [1, 2, 3])
+def test_fusion_modes_parity_select_and_repeat(zz, fusion):
+    zz.set_fusion(fusion)
+    try:
+        S, T, _ = gen.config("C2", seed=0)
+        X0, e0, info = solve(zz, S, T, mb=64)       # 32 tiles: groups of 2 / 3 with remainders
+        if fusion > 1:
+            assert info["fused_pairs"] >= 8
+        check_against_oracle(S, T, X0, e0)
+        X1, e1, _ = solve(zz, S, T, mb=64)
+        assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
+        # a selection whose first active tile opens mid-group: bitwise the full solve's columns
+        m = S.shape[0]
+        for lo in (m - 200, m - 130, m - 70):
+            sel = np.zeros(m, np.int32)
+            sel[lo::37] = 1
+            sel[5:60:9] = 1
+            Xs, es, _ = solve(zz, S, T, mb=64, select=sel)
+            lay_f = checks.column_layout(None, None, S)
+            lay_s = checks.column_layout(None, None, S, sel)
+            start = {j: col for col, j, _ in lay_f}
+            for col, j, sz in lay_s:
+                assert np.array_equal(Xs[:, col:col + sz], X0[:, start[j]:start[j] + sz]), (lo, j)
+    finally:
+        zz.set_fusion(3)
+
+
+@pytest.mark.parametrize("fusion", [1, 3])
+def test_fusion_modes_stress(zz, fusion):
+    # the scaling decisions of the grouped steps on a pencil whose unprotected substitution
+    # overflows: finite, scaled, componentwise backward stable
+    zz.set_fusion(fusion)
+    try:
+        S, T = _stress(2000, 1)
+        X, e, info = solve(zz, S, T, mb=64)
+        assert np.isfinite(X).all() and info["n_scaled"] > 0 and (e <= 0).all()
+        ref = oracle.tgevc(S, T)
+        lay = checks.column_layout(None, None, S)
+        w = checks.comp_backward_error(S, T, X, ref["pairs"], lay, S.shape[0])
+        assert w <= 10 * S.shape[0] * U, w
+    finally:
+        zz.set_fusion(3)

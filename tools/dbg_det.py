@@ -17,7 +17,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     print("repeats equal:", eq, "differing columns:", nbad)
     sys.exit(0)
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
-for tag, env in (("nofuse", {"ZZ_FUSE": "0"}), ("fuse", {"ZZ_FUSE": "1"})):
+for tag, env in (("nofuse", {"ZZ_FUSE": "1"}), ("pairs", {"ZZ_FUSE": "2"}), ("triples", {"ZZ_FUSE": "3"})):
     cfg = env.get("CFG", cfg)
     r = subprocess.run([sys.executable, __file__, "child", cfg], env=dict(os.environ, **env), capture_output=True, text=True)
     print(tag, "|", r.stdout.strip(), r.stderr[-300:])
