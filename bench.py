@@ -330,12 +330,15 @@ def main():
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_update"]
             traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            if tr.get("algorithmic_bytes"):
+                res.setdefault("_traffic_alg", tr["algorithmic_bytes"])
             tnote = "DRAM bytes of one k_update launch, " + tr["source"]
         except Exception:
             pass
         res["roofline"] = {"bound": "tensor", "kernel": "k_update (DMMA.8x8x4 FP64 contraction)",
                            "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
-                           "traffic": traffic, "traffic_note": tnote, "peak_source": PEAK_SRC,
+                           "traffic": traffic, "traffic_note": tnote,
+                           "traffic_algorithmic_bytes": res.pop("_traffic_alg", None), "peak_source": PEAK_SRC,
                            "algorithmic_flops_per_launch": F_upd / n_upd_launch,
                            "update_launches_per_step": n_upd_launch,
                            "avg_launch_ms": upd_avg,

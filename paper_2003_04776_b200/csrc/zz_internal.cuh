@@ -129,6 +129,7 @@ struct UpdParams {
   int t0c, nksc;
   const double* Wc;
   int l2hint;        // L2 eviction priorities: C evict_first, W evict_last (set by launch_update)
+  int ngroup;        // N tiles per group of the CTA order (set by launch_update)
 };
 
 // Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.

@@ -310,6 +310,24 @@ struct UT {
   static constexpr int MINB = (WN == 2) ? 2 : 1;
 };
 
+// CTA order: groups of `ng` N tiles; inside a group the M tiles are the slow index and the
+// group's N tiles the fast one.  Consecutive CTAs share one S/T panel block (A reuse in L2)
+// while the group's W columns stay in L2 for the sweep over all M tiles (with three
+// segments W no longer fits L2 whole: the ungrouped order re-read it from DRAM per M tile).
+// ng <= 0: one group (M-major over all N tiles).
+__device__ __forceinline__ void tile_coords(int tile, int n_mtiles, int n_ntl, int ng, int& mt, int& ntl) {
+  if (ng <= 0 || ng >= n_ntl) {
+    mt = tile / n_ntl;
+    ntl = tile % n_ntl;
+    return;
+  }
+  const int per = n_mtiles * ng;          // CTAs of a full group
+  const int g = tile / per, loc = tile - g * per;
+  const int gs = min(ng, n_ntl - g * ng);  // N tiles in this group (the last may be short)
+  mt = loc / gs;
+  ntl = g * ng + loc % gs;
+}
+
 template <int WN, int BOX, int MODE = 0>
 __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
     k_update_t(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
@@ -353,8 +371,10 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
       int g = 0;
       {
         const int tile = blockIdx.x;
-        const int m0 = mbase + (tile / n_ntl) * kBM;
-        const int nb64 = p.ntile0 + (tile % n_ntl) * (C::BN / kBN);   // first 64-column block
+        int mt, ntl;
+        tile_coords(tile, n_mtiles, n_ntl, p.ngroup, mt, ntl);
+        const int m0 = mbase + mt * kBM;
+        const int nb64 = p.ntile0 + ntl * (C::BN / kBN);   // first 64-column block
         const int nblk = min(C::BN / kBN, p.ntile_end - nb64);         // 64-column blocks present
         for (int kc = 0; kc < nkc; ++kc, ++g) {
           const int s = g % kStages;
@@ -396,8 +416,10 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   int g = 0;
   {
     const int tile = blockIdx.x;
-    const int m0 = mbase + (tile / n_ntl) * kBM;
-    const int n0 = (p.ntile0 + (tile % n_ntl) * (C::BN / kBN)) * kBN;
+    int mt, ntl;
+    tile_coords(tile, n_mtiles, n_ntl, p.ngroup, mt, ntl);
+    const int m0 = mbase + mt * kBM;
+    const int n0 = (p.ntile0 + ntl * (C::BN / kBN)) * kBN;
     double acc[4][8][2];
     // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
     int sy[4];
@@ -559,8 +581,11 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
   if (n_mtiles <= 0 || n_ntiles <= 0) return cudaSuccess;
   // ZZ_L2HINT (bits): 1 = W evict_last, 2 = C loads evict_first, 4 = C stores evict_first
   static const int l2hint = getenv("ZZ_L2HINT") ? atoi(getenv("ZZ_L2HINT")) : 7;
+  // ZZ_NGROUP: N tiles per CTA-order group (tile_coords; 0 = ungrouped)
+  static const int ngroup = getenv("ZZ_NGROUP") ? atoi(getenv("ZZ_NGROUP")) : 64;
   UpdParams q = p;
   q.l2hint = l2hint;
+  q.ngroup = ngroup;
   return launch_update_impl(tmS, tmT, q, n_mtiles, n_ntiles, st, ver, persist);
 }
 
