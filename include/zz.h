@@ -86,11 +86,12 @@ int zz_set_tile(int mb);
  * zz_info_t.ms_update.  Adds an event pair per step; used by bench.py for the roofline. */
 int zz_set_timing(int on);
 
-/* Step grouping of the wavefront for this thread's context: 1 = one update launch per step;
- * 2 = pairs of steps share one update of the rows above them with K = 2 tiles;
- * 3 (default) = triples (K = 3 tiles).  Results differ only by summation order (DESIGN.md s.6);
- * groups are fixed by the tile index, so results never depend on `select`.  Tiles of more
- * than 128 rows always run ungrouped.  Returns 0, -1 (k not in 1..3) or -103. */
+/* Step grouping of the wavefront for this thread's context: k consecutive steps share one
+ * update of the rows above them with K = k tiles (1 = the paper's one update per step; 2 =
+ * pairs; 3 = triples; 4 = the default; up to 6).  Results differ only by summation order and by
+ * how conservative the scaling bounds are (DESIGN.md s.6); groups are fixed by the tile
+ * index, so results never depend on `select`.  Tiles of more than 128 rows always run
+ * ungrouped.  Returns 0, -1 (k not in 1..6) or -103. */
 int zz_set_fusion(int k);
 
 /*

@@ -121,7 +121,7 @@ def set_tile(mb):
 
 
 def set_fusion(k):
-    """Step grouping of the wavefront: 1, 2 or 3 (default) consecutive steps per update."""
+    """Step grouping of the wavefront: 1 .. 6 consecutive steps per update (default 4)."""
     _check(load().zz_set_fusion(int(k)), "zz_set_fusion")
 
 

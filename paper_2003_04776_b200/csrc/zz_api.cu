@@ -59,11 +59,12 @@ struct Context {
   int mb = 0;
   int timing = 0;
   // step groups of the wavefront: 1 (none), 2 (pairs) or 3 (triples); zz_set_fusion, ZZ_FUSE
-  int fusion = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 3;
+  int fusion = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 4;
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
-  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, W2, W3, status, tmp, Sc, Tc, Apk, Xi;
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Apk, Xi, egrp;
+  Buf Wx[kMaxGroup - 1];   // the W operands of a step group's later steps
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
   Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
@@ -76,9 +77,10 @@ struct Context {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   ~Context() {}
   void release() {
-    Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W, &W2,
-                  &W3, &status, &tmp, &Sc, &Tc, &Apk, &Xi, &hS, &hT, &hX, &hE};
+    Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
+                  &status, &tmp, &Sc, &Tc, &Apk, &Xi, &egrp, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
+    for (Buf& b : Wx) b.release();
     Xb.release();
     Sl.release();
     Tl.release();
@@ -279,7 +281,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
   CK(c->rows.ensure((sizeof(int) + 1) * (size_t)m + 16));
   CK(c->blks.ensure(sizeof(int) * 3 * (size_t)nb));
-  CK(c->state.ensure(sizeof(unsigned long long) * 3 * (size_t)n));
+  CK(c->state.ensure(sizeof(unsigned long long) * kMaxGroup * (size_t)n));
+  CK(c->egrp.ensure(sizeof(int) * (kMaxGroup - 1) * (size_t)n));
   CK(c->seg.ensure((sizeof(int) + 2 * sizeof(double)) * (size_t)M * n));
   CK(c->norms.ensure(sizeof(double) * 4 * (size_t)M));
   CK(c->W.ensure(sizeof(double) * (size_t)n_ntiles_all * 2 * nks_max * kBN * kBK));
@@ -295,6 +298,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.e_pend = P.col_tile + n;
   P.sY = P.e_pend + n;
   P.e_prev = P.sY + n;
+  P.e_grp = c->egrp.as<int>();
   P.item_col = c->items.as<int>();
   P.real_items = P.item_col + n_items;
   P.pair_items = P.real_items + real_list.size();
@@ -438,7 +442,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     if (r) return r;
   }
   CK(cudaMemsetAsync(P.e_pend, 0, sizeof(int) * n, st));
-  CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * 3 * n, st));
+  CK(cudaMemsetAsync(P.nY, 0, sizeof(unsigned long long) * kMaxGroup * n, st));
   CK(cudaEventRecord(c->e1, st));
   // ---- the wavefront (Algorithm 1 over tile rows, bottom-up) ----
   // X with an odd leading dimension or a base that is not 16-byte aligned: solve into an
@@ -466,10 +470,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   // 128-row band), tile J is solved, and the rows above tile J get both steps' updates in one
   // contraction with K = [tile J | tile I] (twice the K of a single step: half the C-tile
   // traffic and prologue/epilogue per flop).
-  const int fusion = std::max(1, std::min(3, c->fusion));
+  const int fusion = std::max(1, std::min(kMaxGroup, c->fusion));
   const bool can_fuse = fusion > 1 && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
-  CK(c->W2.ensure(c->W.cap));
-  if (fusion == 3) CK(c->W3.ensure(c->W.cap));
+  for (int k = 0; k + 1 < fusion; ++k) CK(c->Wx[k].ensure(c->W.cap));
   int nyb = (M - 1) & 1;   // nY buffer holding the pending max for the next decision
   static const bool dbg_sync = getenv("ZZ_DEBUG_SYNC") != nullptr;
   auto dbg = [&](const char* what, int I) -> int {
@@ -522,22 +525,22 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.P = P;
       d2.nY_in = dp.nY_in;
       d2.Wout = Wout;
+      d2.grp_slot = -1;
       if (fuse_from) {
-        // step-group role (zz_diag3.cu): fused = 1 last step of a pair, 2 middle step of a
-        // triple (band decision, nY buffer 2), 3 last step of a triple; reset_band: first
-        // step of a triple
+        // role in a step group (zz_diag3.cu): first (grp_slot 0), middle (fused 2), last (3)
         d2.fused = fuse_from->fused;
-        d2.Iprev = fuse_from->Iprev;
-        d2.cs_prev = fuse_from->cs_prev;
+        d2.grp_slot = fuse_from->grp_slot;
+        d2.n_band_reset = fuse_from->n_band_reset;
+        d2.band_in = fuse_from->band_in;
+        d2.n_prev = fuse_from->n_prev;
+        for (int k = 0; k < kMaxGroup - 1; ++k) {
+          d2.prev_I[k] = fuse_from->prev_I[k];
+          d2.prev_cs[k] = fuse_from->prev_cs[k];
+          d2.prev_nks[k] = fuse_from->prev_nks[k];
+          d2.prev_W[k] = fuse_from->prev_W[k];
+        }
         d2.zero_pend_end = fuse_from->zero_pend_end;
-        d2.Wprev = fuse_from->Wprev;
-        d2.nks_prev = fuse_from->nks_prev;
-        d2.Jprev = fuse_from->Jprev;
-        d2.cs_prev2 = fuse_from->cs_prev2;
-        d2.Wprev2 = fuse_from->Wprev2;
-        d2.nks_prev2 = fuse_from->nks_prev2;
-        d2.reset_band = fuse_from->reset_band;
-        if (d2.fused == 2) d2.nY_in = 2;
+        if (d2.fused == 2) d2.nY_in = d2.band_in;
       }
       CK(launch_diag3(d2, st));
     } else {
@@ -550,7 +553,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     const int n_n = ceil_div(n_sel, kBN) - up.ntile0;
     if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));
     CK(launch_update(&tmS, &tmT, up, n_m, n_n, st));
-    if (int r = dbg(up.nksb ? "fused update" : (up.row_lo ? "thin update" : "update"), up.t0 / std::max(mb, 1))) return r;
+    if (int r = dbg(up.nxs ? "fused update" : (up.row_lo ? "thin update" : "update"), up.t0 / std::max(mb, 1))) return r;
     if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], st));
     n_upd++;
     launches++;
@@ -591,80 +594,67 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     }
     const int J = I - 1, K = I - 2;
     auto nks_of = [&](int t) { return ceil_div(ts[t + 1] - ts[t], kBK); };
-    if (len == 3) {
-      // ---- three-step group (I, J, K): thin updates of the band of tiles J, K; one update
-      // above tile K with K = [tile K | tile J | tile I] ----
-      Diag2Params oi;
-      memset(&oi, 0, sizeof(oi));
-      oi.reset_band = 1;
-      if ((r = diag(I, P.W, &oi))) return r;
-      UpdParams th = base_up(I);            // rows of tiles K and J; band max over tile K's rows
-      th.row_lo = ts[K];
-      th.max_row = ts[J];
-      th.nY_out = P.nY + 2 * (size_t)n;
-      if ((r = update(th, ceil_div(ts[I] - (ts[K] & ~1), kBM)))) return r;
-      if ((r = panel_ready(J))) return r;
-      Diag2Params oj;
-      memset(&oj, 0, sizeof(oj));
-      oj.fused = 2;
-      if ((r = diag(J, c->W2.as<double>(), &oj))) return r;
-      UpdParams tj = base_up(J);            // rows of tile K with W_J
-      tj.row_lo = ts[K];
-      tj.max_row = 0;
-      tj.W = c->W2.as<double>();
-      if ((r = update(tj, ceil_div(ts[J] - (ts[K] & ~1), kBM)))) return r;
-      if ((r = panel_ready(K))) return r;
-      Diag2Params ok;
-      memset(&ok, 0, sizeof(ok));
-      ok.fused = 3;
-      ok.Iprev = I;
-      ok.cs_prev = cs[I];
-      ok.Jprev = J;
-      ok.cs_prev2 = cs[J];
-      ok.zero_pend_end = cs[I + 1];
-      ok.Wprev = P.W;
-      ok.nks_prev = nks_of(I);
-      ok.Wprev2 = c->W2.as<double>();
-      ok.nks_prev2 = nks_of(J);
-      if ((r = diag(K, c->W3.as<double>(), &ok))) return r;
-      UpdParams fu = base_up(K);
-      fu.W = c->W3.as<double>();
-      fu.first_end = cs[I + 1];             // tips of I, J and K start from zero pending rows
-      fu.t0b = ts[J]; fu.nksb = nks_of(J); fu.Wb = c->W2.as<double>();
-      fu.t0c = ts[I]; fu.nksc = nks_of(I); fu.Wc = P.W;
-      if ((r = update(fu, ceil_div(ts[K], kBM)))) return r;
+    if (len >= 2) {
+      // ---- a step group (I, I-1, ..., L = I-len+1): diag of each step, thin updates of the
+      // group's own band (the rows of its later tiles) after every step but the last, and one
+      // update of all rows above tile L with K = [tile L | ... | tile I] ----
+      const int L = I - len + 1;
+      double* Wg[kMaxGroup];
+      Wg[0] = P.W;
+      for (int k = 1; k < len; ++k) Wg[k] = c->Wx[k - 1].as<double>();
+      for (int sgi = 0; sgi < len; ++sgi) {
+        const int X = I - sgi;
+        if (sgi > 0 && (r = panel_ready(X))) return r;
+        Diag2Params o;
+        memset(&o, 0, sizeof(o));
+        if (sgi == 0) {
+          o.fused = 0;
+          o.grp_slot = 0;
+          o.n_band_reset = len - 2;
+        } else if (sgi < len - 1) {
+          o.fused = 2;
+          o.grp_slot = sgi;
+          o.band_in = 2 + (sgi - 1);
+        } else {
+          o.fused = 3;
+          o.grp_slot = -1;
+          o.n_prev = len - 1;
+          for (int k = 0; k < len - 1; ++k) {
+            o.prev_I[k] = I - k;
+            o.prev_cs[k] = cs[I - k];
+            o.prev_nks[k] = nks_of(I - k);
+            o.prev_W[k] = Wg[k];
+          }
+          o.zero_pend_end = cs[I + 1];       // tips of the group start from zero pending rows
+        }
+        if ((r = diag(X, Wg[sgi], &o))) return r;
+        if (sgi < len - 1) {
+          UpdParams th = base_up(X);         // rows of the group's tiles below X with W_X
+          th.row_lo = ts[L];
+          th.W = Wg[sgi];
+          if (sgi + 1 < len - 1) {           // band maximum for the next (middle) step
+            th.max_row = ts[X - 1];
+            th.nY_out = P.nY + (size_t)(2 + sgi) * n;
+          } else {
+            th.max_row = 0;
+          }
+          if ((r = update(th, ceil_div(ts[X] - (ts[L] & ~1), kBM)))) return r;
+        }
+      }
+      UpdParams fu = base_up(L);
+      fu.W = Wg[len - 1];
+      fu.first_end = cs[I + 1];
+      fu.nxs = len - 1;
+      for (int e = 0; e < len - 1; ++e) {    // tiles L+1, ..., I after tile L
+        const int X = L + 1 + e;
+        fu.xt0[e] = ts[X];
+        fu.xnks[e] = nks_of(X);
+        fu.xW[e] = Wg[I - X];
+      }
+      if ((r = update(fu, ceil_div(ts[L], kBM)))) return r;
       nyb = 1 - nyb;
       ++n_fused;
-      I -= 3;
-      continue;
-    }
-    if (len == 2) {
-      // ---- fused pair (I, J) ----
-      if ((r = diag(I, P.W, nullptr))) return r;
-      UpdParams thin = base_up(I);          // rows of tile J only, no column maximum
-      thin.row_lo = ts[J];
-      thin.max_row = 0;
-      if ((r = update(thin, ceil_div(ts[I] - (ts[J] & ~1), kBM)))) return r;
-      if ((r = panel_ready(J))) return r;
-      Diag2Params oj;
-      memset(&oj, 0, sizeof(oj));
-      oj.fused = 1;
-      oj.Iprev = I;
-      oj.cs_prev = cs[I];
-      oj.zero_pend_end = cs[I + 1];
-      oj.Wprev = P.W;
-      oj.nks_prev = nks_of(I);
-      if ((r = diag(J, c->W2.as<double>(), &oj))) return r;
-      UpdParams fu = base_up(J);            // rows above tile J, K = [tile J | tile I]
-      fu.W = c->W2.as<double>();
-      fu.first_end = cs[I + 1];             // tips of I and J start from zero pending rows
-      fu.t0b = ts[I];
-      fu.nksb = nks_of(I);
-      fu.Wb = P.W;
-      if ((r = update(fu, ceil_div(ts[J], kBM)))) return r;
-      nyb = 1 - nyb;
-      ++n_fused;
-      I -= 2;
+      I -= len;
       continue;
     }
     if ((r = diag(I, P.W, nullptr))) return r;
@@ -849,7 +839,7 @@ int zz_set_tile(int mb) {
 
 int zz_set_fusion(int k) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
-  if (k < 1 || k > 3) return -1;
+  if (k < 1 || k > kMaxGroup) return -1;
   g_ctx->fusion = k;
   return 0;
 }

@@ -523,35 +523,34 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       P.nrmh_seg[so] = lh;
     }
     if (p.do_update && p.fused == 3) {
-      // last step K of a three-step group (I, J = I - 1, K = I - 2): one update of the rows
-      // above tile K (region R, still at the exponent e_p of before step I) with all three
-      // tiles, K = [tile K | tile J | tile I].  W_I is at e1 (step I's decision), W_J at
-      // e2 = e_pend (step J's band decision, reading R5 on tile K's rows), W_K at es.  The
-      // decision bounds all four terms as the two-step one does:
+      // last step L of a step group (I, I-1, ..., L): one update of the rows above tile L
+      // (region R, still at the exponent e_p it had before step I) with all the group's
+      // tiles, K = [tile L | tile L+1 | ... | tile I].  The W of an earlier step X is at the
+      // exponent e_X of its decision (e_grp), W_L at es; the band rows of tile L are at
+      // ep = the last middle decision's exponent.  The decision bounds every term at once
+      // (Alg. 3 with the sum of the panels' norms and the largest aligned segment norm, R5):
       //   2^(ef-e_p) y^_R + sum_X tau_X 2^(ef-e_X) x^_X <= 2^(ef-g)(y^ + (sum tau) max_X x^_X 2^(g-e_X)) <= Omega
-      const bool act_i = c0 >= p.cs_prev;                     // active at step I
-      const bool act_j = c0 >= p.cs_prev2;                    // active at step J
-      const int e2 = ep;
-      const int e_p = act_i ? P.e_prev[c] : 0;                // written by step I only
-      const int e1 = act_i ? e2 - P.sY[c] : 0;                // step J's shift of the band: e2 - e1
+      // A column not active at an earlier step has no term (and zero W) for it; a column
+      // active only at L gets exactly the single-step decision.
+      const bool act_first = p.n_prev > 0 && c0 >= p.prev_cs[0];
+      const int e_p = act_first ? P.e_prev[c] : 0;            // written by the group's first step
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
       double nyv = 0.0;
-      if (c0 >= p.zero_pend_end) {                            // not a tip of I, J or K
+      if (c0 >= p.zero_pend_end) {                            // not a tip of the group
         nyv = __longlong_as_double((long long)nyi[c0]);
         if (PAIR) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
       }
-      const int g0 = min(e2, es);
+      const int g0 = min(ep, es);
       double xh = scale2k(lm, g0 - es);
       double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
-      if (act_j) {
-        const long long sp = (long long)p.Jprev * p.n_sel + c;
-        xh = dmaxd(xh, scale2k(P.nrm_seg[sp], g0 - P.e_seg[sp]));
-        tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Jprev]), __dmul_rn(ab, P.cT[p.Jprev])));
-      }
-      if (act_i) {
-        const long long sp = (long long)p.Iprev * p.n_sel + c;
-        xh = dmaxd(xh, scale2k(P.nrm_seg[sp], g0 - P.e_seg[sp]));
-        tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Iprev]), __dmul_rn(ab, P.cT[p.Iprev])));
+      // earlier steps nearest first (tile L+1, ..., tile I): the order of the terms
+#pragma unroll
+      for (int k = kMaxGroup - 2; k >= 0; --k) {
+        if (k < p.n_prev && c0 >= p.prev_cs[k]) {
+          const long long sp = (long long)p.prev_I[k] * p.n_sel + c;
+          xh = dmaxd(xh, scale2k(P.nrm_seg[sp], g0 - P.e_seg[sp]));
+          tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.prev_I[k]]), __dmul_rn(ab, P.cT[p.prev_I[k]])));
+        }
       }
       const double yh = scale2k(nyv, g0 - e_p);
       const int ef = g0 + protect_update(yh, tau, xh);
@@ -561,82 +560,31 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         P.e_pend[c] = ef;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
       }
-      // W_I and W_J of this column brought to ef (rare), or zero where the column was not
+      // each earlier W of this column brought to ef (rare), or zero where the column was not
       // active at that step (stale entries)
-      if (!act_i || ef != e1) {
-        const long long tstr = (long long)(2 * p.nks_prev) * (kBN * kBK);
-        const long long hf = (long long)p.nks_prev * (kBN * kBK);
-        double* Wp = p.Wprev + (long long)(c / kBN) * tstr + (c % kBN) * 4;
-        for (int r = t; r < p.nks_prev * kBK; r += 4) {
-          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
-          Wp[off] = act_i ? scale2k(Wp[off], ef - e1) : 0.0;
-          Wp[off + hf] = act_i ? scale2k(Wp[off + hf], ef - e1) : 0.0;
-        }
-      }
-      if (!act_j || ef != e2) {
-        const long long tstr = (long long)(2 * p.nks_prev2) * (kBN * kBK);
-        const long long hf = (long long)p.nks_prev2 * (kBN * kBK);
-        double* Wp = p.Wprev2 + (long long)(c / kBN) * tstr + (c % kBN) * 4;
-        for (int r = t; r < p.nks_prev2 * kBK; r += 4) {
-          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
-          Wp[off] = act_j ? scale2k(Wp[off], ef - e2) : 0.0;
-          Wp[off + hf] = act_j ? scale2k(Wp[off + hf], ef - e2) : 0.0;
-        }
-      }
-    } else if (p.do_update && p.fused == 1) {
-      // second step J of a fused pair (I, J = I - 1): one update of the rows above tile J with
-      // both tiles (K = [tile J | tile I]).  Those rows are still at the exponent e_p they had
-      // before step I (step I only updated tile J's rows, the thin update); step I's W_I is at
-      // e1 = e_pend.  The decision bounds all three terms (Alg. 3 with the sum of the two
-      // panels' norms and the larger of the two aligned segment norms, R5):
-      //   2^(ef-e_p) y^ + 2^(ef-e1) tau_I |W_I| + tau_J 2^(ef-e_J) x^_J <= Omega.
-      const bool act_prev = c0 >= p.cs_prev;                  // active at step I
-      const int e1 = ep;
-      const int e_p = act_prev ? P.e_prev[c] : 0;              // written by step I only
-      const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
-      double nyv = 0.0;
-      if (c0 >= p.zero_pend_end) {                            // not a tip of I or J
-        nyv = __longlong_as_double((long long)nyi[c0]);
-        if (PAIR) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
-      }
-      double xI = 0.0;
-      int eI = 0;
-      if (act_prev) {
-        const long long sp = (long long)p.Iprev * p.n_sel + c;
-        xI = P.nrm_seg[sp];
-        eI = P.e_seg[sp];
-      }
-      const int g0 = min(e1, es);
-      const double yh = scale2k(nyv, g0 - e_p);
-      const double xh = dmaxd(act_prev ? scale2k(xI, g0 - eI) : 0.0, scale2k(lm, g0 - es));
-      // (a column not active at step I has no tile-I term: its decision is then exactly the
-      // single-step one)
-      double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
-      if (act_prev) tau = __dadd_rn(tau, __dadd_rn(__dmul_rn(beta, P.cS[p.Iprev]), __dmul_rn(ab, P.cT[p.Iprev])));
-      const int ef = g0 + protect_update(yh, tau, xh);
-      sx = ef - es;
-      if (t == 0) {
-        P.sY[c] = ef - e_p;
-        P.e_pend[c] = ef;
-        P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
-      }
-      // W_I of this column: rescaled to ef (rare), or zero for a tip of J (stale entries)
-      if (!act_prev || ef != e1) {
-        const long long tstr = (long long)(2 * p.nks_prev) * (kBN * kBK);
-        const long long hf = (long long)p.nks_prev * (kBN * kBK);
-        double* Wp = p.Wprev + (long long)(c / kBN) * tstr + (c % kBN) * 4;
-        for (int r = t; r < p.nks_prev * kBK; r += 4) {
-          const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
-          Wp[off] = act_prev ? scale2k(Wp[off], ef - e1) : 0.0;
-          Wp[off + hf] = act_prev ? scale2k(Wp[off + hf], ef - e1) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kMaxGroup - 1; ++k) {
+        if (k < p.n_prev) {
+          const bool act = c0 >= p.prev_cs[k];
+          const int ek = act ? P.e_grp[(long long)k * p.n_sel + c] : 0;
+          if (!act || ef != ek) {
+            const long long tstr = (long long)(2 * p.prev_nks[k]) * (kBN * kBK);
+            const long long hf = (long long)p.prev_nks[k] * (kBN * kBK);
+            double* Wp = p.prev_W[k] + (long long)(c / kBN) * tstr + (c % kBN) * 4;
+            for (int r = t; r < p.prev_nks[k] * kBK; r += 4) {
+              const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
+              Wp[off] = act ? scale2k(Wp[off], ef - ek) : 0.0;
+              Wp[off + hf] = act ? scale2k(Wp[off + hf], ef - ek) : 0.0;
+            }
+          }
         }
       }
     } else if (p.do_update) {
       // Alg. 3 with Alg. 2, reading R5; pending max of the column
       // (pairs: of both columns)
-      // (fused == 2: the middle step J of a three-step group -- the decision covers tile K's
-      // rows only, whose maximum the thin update of step I left in buffer nY_in = 2; the
-      // exponent e_p of the rows above tile K stays in e_prev for step K)
+      // (fused == 2: a middle step of a group -- the decision covers the group's rows below
+      // it only, whose maximum the previous thin update left in band buffer nY_in; the
+      // exponent e_p of the rows above the group stays in e_prev for the last step)
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
       double nyv = tip ? 0.0 : __longlong_as_double((long long)nyi[c0]);
       if (PAIR && !tip) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
@@ -650,7 +598,8 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         if (p.fused != 2) P.e_prev[c] = ep;   // the pending exponent before this step (read by a fused J/K)
         P.e_pend[c] = en;
         if (p.fused != 2) P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
-        if (p.reset_band) P.nY[2LL * p.n_sel + c] = 0ull;   // the band maximum of a three-step group
+        if (p.grp_slot >= 0) P.e_grp[(long long)p.grp_slot * p.n_sel + c] = en;   // exponent of this W
+        for (int k = 0; k < p.n_band_reset; ++k) P.nY[(2LL + k) * p.n_sel + c] = 0ull;   // band maxima
       }
     }
   }

@@ -77,8 +77,9 @@ struct DevPlan {
   // robustness state
   int* e_pend;        // per column: exponent of the pending (not yet solved) rows
   int* sY;            // per column: exponent shift of the pending rows at this step
-  int* e_prev;        // per column: pending exponent before the last decision (fused pairs)
-  unsigned long long* nY;   // 3 x n_sel: max |pending| (double bits), double buffered + band
+  int* e_prev;        // per column: pending exponent before a group's first decision
+  int* e_grp;         // (kMaxGroup - 1) x n_sel: exponent of each earlier step's W in a group
+  unsigned long long* nY;   // kMaxGroup x n_sel: max |pending| (double bits), 2 alternating + band buffers
   int* e_seg;         // M x n_sel: exponent of each solved segment
   double* nrm_seg;    // M x n_sel: max(|Re|,|Im|) of the segment
   double* nrmh_seg;   // M x n_sel: max(|x|/2 + |y|/2) (pair) or |x|/2 (real)
@@ -104,6 +105,9 @@ struct DiagParams {
   int nY_in;         // which nY buffer holds the pending max of this step
 };
 
+// steps per group of the wavefront (zz_set_fusion): one update per group of this many steps
+constexpr int kMaxGroup = 6;
+
 struct UpdParams {
   int rows;          // ts_I: rows [0, rows) are updated
   int max_row;       // ts_{I-1}: rows [0, max_row) form the next pending region
@@ -121,13 +125,11 @@ struct UpdParams {
   int vec;           // 16-byte aligned X access possible
   const double* Apk; // S/T panel packed in fragment order (update_packs()), or null
   int row_lo;        // rows [row_lo, rows) are updated (0, or a tile start for the thin update)
-  // optional second K segment (two-step fused update): S/T columns of tile t0b (nksb chunks
-  // per part) against Wb; nksb = 0 if absent
-  int t0b, nksb;
-  const double* Wb;
-  // optional third segment (three-step group): tile t0c, nksc chunks per part, Wc
-  int t0c, nksc;
-  const double* Wc;
+  // further K segments of a step group's update (MODE 1): S/T columns of tile xt0[e]
+  // (xnks[e] chunks per part) against xW[e], in this order after (t0, nks, W)
+  int nxs;
+  int xt0[kMaxGroup - 1], xnks[kMaxGroup - 1];
+  const double* xW[kMaxGroup - 1];
   int l2hint;        // L2 eviction priorities: C evict_first, W evict_last (set by launch_update)
   int ngroup;        // N tiles per group of the CTA order (set by launch_update)
 };
@@ -153,19 +155,19 @@ struct Diag2Params {
   double* Wout;            // where this step's B operand W goes
   // second step of a fused pair (I, J = I - 1): the update of the rows above tile J is done
   // once with both tiles; tile I's step left its W in Wprev (nks_prev chunks per part)
+  // role in a step group (I, I-1, ..., L) whose rows above tile L get one update with all
+  // the group's tiles: fused = 0 a single step or the group's first (grp_slot = 0, it zeroes
+  // n_band_reset band buffers nY[2..]); 2 a middle step (a band decision for the group's rows
+  // below it, band maximum in nY[band_in], exponent to e_grp[grp_slot]); 3 the last step L
+  // (the decision for the rows above L with the n_prev earlier steps' terms)
   int fused;
-  int Iprev;               // I
-  int cs_prev;             // columns >= cs_prev were active at step I
-  int zero_pend_end;       // columns < zero_pend_end (tips of I and J) have no pending rows
-  double* Wprev;
-  int nks_prev;
-  // three-step groups (I, J = I-1, K = I-2): fused = 2 marks step J (band decision on tile
-  // K's rows, nY_in = 2), fused = 3 step K (one update above tile K with all three tiles);
-  // Jprev/cs_prev2/Wprev2/nks_prev2 describe step J for step K; reset_band (step I) zeroes
-  // the band-maximum buffer nY[2]
-  int Jprev, cs_prev2, nks_prev2;
-  double* Wprev2;
-  int reset_band;
+  int grp_slot;            // -1: not recorded
+  int n_band_reset;
+  int band_in;
+  int n_prev;
+  int prev_I[kMaxGroup - 1], prev_cs[kMaxGroup - 1], prev_nks[kMaxGroup - 1];
+  double* prev_W[kMaxGroup - 1];
+  int zero_pend_end;       // columns < zero_pend_end (tips of the group) have no pending rows
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)

@@ -343,16 +343,19 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // MODE 1 (two-step fused update): a second K segment; MODE 2 (thin update): first row row_lo
   constexpr bool SEG2 = MODE == 1;
-  // K chunks: segment a, then b, then c (MODE 1; a step group of two or three tiles)
-  const int nkca = 2 * p.nks, nkcb = SEG2 ? 2 * p.nksb : 0, nkcc = SEG2 ? 2 * p.nksc : 0;
-  const int nkc = nkca + nkcb + nkcc;
+  // K chunks: segment 0 (t0, nks, W), then the group's further segments (MODE 1)
+  const int nkca = 2 * p.nks;
+  int nkc = nkca;
+  if (SEG2) {
+#pragma unroll
+    for (int e = 0; e < kMaxGroup - 1; ++e) nkc += (e < p.nxs) ? 2 * p.xnks[e] : 0;
+  }
   const int n_ntl = n_tiles / n_mtiles;
   const int row_lo = (MODE == 2) ? p.row_lo : 0;
   const int mbase = row_lo & ~1;                         // 16-byte aligned first row pair
   // W is stored per 64-column block: [ntile64][kc][BK/4][64][4] (per segment)
   const long long wtile = (long long)nkca * (kBN * kBK);
-  const long long wtileb = (long long)(2 * p.nksb) * (kBN * kBK);
-  const long long wtilec = (long long)(2 * p.nksc) * (kBN * kBK);
+
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -380,11 +383,27 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           const int s = g % kStages;
           if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
           mbar_expect_tx(&full[s], kABytes + nblk * kBBytes);
-          const int sg = !SEG2 ? 0 : (kc < nkca ? 0 : (kc < nkca + nkcb ? 1 : 2));   // segment
-          const int kl = kc - (sg == 0 ? 0 : (sg == 1 ? nkca : nkca + nkcb));   // chunk within it
-          const int nks_s = sg == 0 ? p.nks : (sg == 1 ? p.nksb : p.nksc);
+          // segment of chunk kc (static indices: the parameter arrays stay in constant space)
+          int kl = kc, nks_s = p.nks, t0_s = p.t0;
+          const double* w_s = p.W;
+          if (SEG2 && kc >= nkca) {
+            int base = nkca;
+            bool found = false;
+#pragma unroll
+            for (int e = 0; e < kMaxGroup - 1; ++e) {
+              const int n2 = (e < p.nxs) ? 2 * p.xnks[e] : 0;
+              if (!found && kc < base + n2) {
+                found = true;
+                kl = kc - base;
+                nks_s = p.xnks[e];
+                t0_s = p.xt0[e];
+                w_s = p.xW[e];
+              }
+              base += n2;
+            }
+          }
           const CUtensorMap* tm = (kl < nks_s) ? &tmS : &tmT;
-          const int kcol = (sg == 0 ? p.t0 : (sg == 1 ? p.t0b : p.t0c)) + (kl % nks_s) * kBK;
+          const int kcol = t0_s + (kl % nks_s) * kBK;
           double* a = sA + s * (kBM * kBK);
           if (BOX == 0) {
             // packed panel (k_pack): one 16 KB bulk copy per stage
@@ -397,9 +416,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
           }
           for (int q = 0; q < nblk; ++q)
             bulk_load_h(sB + s * (C::BN * kBK) + q * (kBN * kBK),
-                        (sg == 0 ? p.W + (long long)(nb64 + q) * wtile
-                                 : (sg == 1 ? p.Wb + (long long)(nb64 + q) * wtileb
-                                            : p.Wc + (long long)(nb64 + q) * wtilec)) +
+                        w_s + (long long)(nb64 + q) * ((long long)(2 * nks_s) * (kBN * kBK)) +
                             (long long)kl * (kBN * kBK),
                         kBBytes, &full[s], pol_w);
         }
@@ -593,7 +610,7 @@ static cudaError_t launch_update_impl(const CUtensorMap* tmS, const CUtensorMap*
                                       int n_mtiles, int n_ntiles, cudaStream_t st, int ver, int persist) {
   // the template kernels move C in 16-byte pairs: X 16-byte aligned with an even ldx
   if (ver == 2 && p.vec) {
-    if (p.nksb > 0) return launch_t<2, 8, 1>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
+    if (p.nxs > 0) return launch_t<2, 8, 1>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
     if (p.row_lo > 0) return launch_t<2, 8, 2>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
     return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
   }
