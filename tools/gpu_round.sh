@@ -17,7 +17,7 @@ if [ "${NCU:-1}" = "1" ]; then
   CMD2="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu"
   timeout 600 $CMD2 > $OUT/${TAG}_plain2.log 2>&1 &&
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-      -k regex:k_update_tILi2ELi8ELi1E -s 40 -c 1 \
+      -k regex:k_update_tILi2ELi8ELi1E -s 30 -c 1 \
       -o $OUT/${TAG}_update $CMD2 > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu update exit $?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_diag -s 150 -c 1 \
       -o $OUT/${TAG}_diag $CMD2 > $OUT/${TAG}_ncu_diag.log 2>&1; echo "ncu diag exit $?"
