@@ -143,6 +143,13 @@ def test_error_codes(zz):
     assert ei.value.status == -104
 
 
+def test_set_fusion_arguments(zz):
+    lib = zz.load()
+    assert lib.zz_set_fusion(0) == -1 and lib.zz_set_fusion(7) == -1
+    for k in (1, 6, 4):
+        assert lib.zz_set_fusion(k) == 0
+
+
 def test_select_subsets_bitwise(zz):
     S, T, _ = gen.config("C2", seed=1)
     m = S.shape[0]
