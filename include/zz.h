@@ -60,8 +60,8 @@ typedef struct zz_info {
   int prescaled;      /* 1 if S or T was pre-scaled by a power of two (reading R6) */
   int update_launches;     /* robust-update kernel launches */
   int total_launches;      /* all kernel launches of the call */
-  int fused_pairs;         /* step pairs whose updates ran as one two-tile contraction */
-  int reserved;
+  int fused_pairs;         /* step groups whose updates ran as one multi-tile contraction */
+  int lookahead_redo;      /* 1 if the lookahead schedule had to be recomputed without it */
   double ms_setup;         /* structure scan, pairs, norms */
   double ms_steps;         /* the wavefront (diagonal solves + updates) */
   double ms_normalize;     /* consistency and normalisation */
@@ -93,6 +93,15 @@ int zz_set_timing(int on);
  * index, so results never depend on `select`.  Tiles of more than 128 rows always run
  * ungrouped.  Returns 0, -1 (k not in 1..6) or -103. */
 int zz_set_fusion(int k);
+
+/* Lookahead schedule: the chain of diagonal solves of a step group runs on a high-priority
+ * stream beside the bulk of the previous group's update (DESIGN.md s.6 "Lookahead").  The
+ * first decision of a group then uses a recorded upper bound of the pending rows instead of
+ * their measured maximum; where that bound would make it scale, the call is recomputed
+ * without lookahead (zz_info_t.lookahead_redo), so results are always those of the plain
+ * schedule, bit for bit.  mode 0 = off, 1 = automatic (default: on for m >= 4096 unless a
+ * panel norm exceeds 2^64), 2 = on whenever step groups are used.  Returns 0, -1 or -103. */
+int zz_set_lookahead(int mode);
 
 /*
  * zz_tgevc: selected right eigenvectors on the device.

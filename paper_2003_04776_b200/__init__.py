@@ -27,7 +27,7 @@ STATUS = {
     -106: "unsupported tile size",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -44,7 +44,7 @@ class Info(ctypes.Structure):
                 ("n_tiles", ctypes.c_int), ("n_scaled", ctypes.c_int), ("min_exp", ctypes.c_int),
                 ("n_indefinite", ctypes.c_int), ("prescaled", ctypes.c_int),
                 ("update_launches", ctypes.c_int), ("total_launches", ctypes.c_int),
-                ("fused_pairs", ctypes.c_int), ("reserved", ctypes.c_int),
+                ("fused_pairs", ctypes.c_int), ("lookahead_redo", ctypes.c_int),
                 ("ms_setup", ctypes.c_double), ("ms_steps", ctypes.c_double),
                 ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double),
                 ("ms_back", ctypes.c_double)]
@@ -79,6 +79,7 @@ def load(build_if_missing=True):
         "zz_set_tile": ([ci], ci),
         "zz_set_timing": ([ci], ci),
         "zz_set_fusion": ([ci], ci),
+        "zz_set_lookahead": ([ci], ci),
         "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_back": ([ci, vp, ci, vp, ci, vp, vp, ci, vp, ci, vp], ci),
@@ -123,6 +124,11 @@ def set_tile(mb):
 def set_fusion(k):
     """Step grouping of the wavefront: 1 .. 6 consecutive steps per update (default 4)."""
     _check(load().zz_set_fusion(int(k)), "zz_set_fusion")
+
+
+def set_lookahead(mode):
+    """Lookahead schedule: 0 off, 1 automatic (default), 2 on (include/zz.h)."""
+    _check(load().zz_set_lookahead(int(mode)), "zz_set_lookahead")
 
 
 def set_timing(on):

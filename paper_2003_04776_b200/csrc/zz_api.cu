@@ -60,11 +60,19 @@ struct Context {
   int timing = 0;
   // step groups of the wavefront: 1 (none), 2 (pairs) or 3 (triples); zz_set_fusion, ZZ_FUSE
   int fusion = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 4;
+  // lookahead (ZZ_LOOKAHEAD): the chain of solves runs on a high-priority stream beside the
+  // bulk of the previous group's update (DESIGN.md s.6 "Lookahead")
+  int lookahead = getenv("ZZ_LOOKAHEAD") ? atoi(getenv("ZZ_LOOKAHEAD")) : 1;
+  cudaStream_t hi = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<cudaEvent_t> ev_la;
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
   Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Apk, Xi, egrp;
   Buf Wx[kMaxGroup - 1];   // the W operands of a step group's later steps
+  Buf Wy[kMaxGroup];       // second set (lookahead: groups alternate between the sets)
+  Buf sYb, nYb;            // second sY set; per-column bound of the pending rows (lookahead)
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
   Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
@@ -81,6 +89,15 @@ struct Context {
                   &status, &tmp, &Sc, &Tc, &Apk, &Xi, &egrp, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     for (Buf& b : Wx) b.release();
+    for (Buf& b : Wy) b.release();
+    sYb.release();
+    nYb.release();
+    for (cudaEvent_t e : ev_la) cudaEventDestroy(e);
+    ev_la.clear();
+    if (ev_in) { cudaEventDestroy(ev_in); cudaEventDestroy(ev_out); }
+    ev_in = ev_out = nullptr;
+    if (hi) cudaStreamDestroy(hi);
+    hi = nullptr;
     Xb.release();
     Sl.release();
     Tl.release();
@@ -299,6 +316,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.sY = P.e_pend + n;
   P.e_prev = P.sY + n;
   P.e_grp = c->egrp.as<int>();
+  CK(c->nYb.ensure(sizeof(double) * (size_t)n));
+  P.nYb = c->nYb.as<double>();
   P.item_col = c->items.as<int>();
   P.real_items = P.item_col + n_items;
   P.pair_items = P.real_items + real_list.size();
@@ -382,6 +401,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   // ---- a2 pairs, a3 norms (second host sync: status + pre-scale test) ----
   // (host-staged path: per panel inside the wavefront, checked after it)
   if (hs) CK(cudaMemsetAsync(P.cS, 0, sizeof(double) * 4 * M, st));
+  double panel_max = 0.0;   // largest panel norm (the lookahead heuristic below)
   for (int pass = 0; pass < 2 && !hs; ++pass) {
     CK(cudaMemsetAsync(P.cS, 0, sizeof(double) * 4 * M, st));
     CK(launch_pairs(Su, ldsu, Tu, ldtu, 0, nb, P, st));
@@ -397,6 +417,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       return kind == 1 ? ZZ_ERR_NONFINITE : bs[p] + 1;
     }
     info.n_indefinite = stat[2];
+    for (int I = 0; I < M; ++I) panel_max = std::max(panel_max, std::max(nrm[I], nrm[M + I]));
     if (pass == 1) break;
     // pre-scale test (reading R6): every row sum of |S| is <= sum_J cS[J] + max_J dS[J]
     double bS = 0, bT = 0, mdS = 0, mdT = 0;
@@ -459,9 +480,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     ldx = ldi;
   }
   const int vec = ((ldx & 1) == 0) && aligned16(X);
-  if (c->timing && (int)c->ev.size() < 2 * M) {
+  if (c->timing && (int)c->ev.size() < 4 * M) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
-    c->ev.assign(2 * (size_t)M, nullptr);
+    c->ev.assign(4 * (size_t)M, nullptr);
     for (auto& e : c->ev) cudaEventCreate(&e);
   }
   int n_upd = 0, n_fused = 0;
@@ -473,6 +494,41 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   const int fusion = std::max(1, std::min(kMaxGroup, c->fusion));
   const bool can_fuse = fusion > 1 && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
   for (int k = 0; k + 1 < fusion; ++k) CK(c->Wx[k].ensure(c->W.cap));
+  // Lookahead: the chain of solves and band updates runs on a high-priority stream `ms`; the
+  // bulk of each group's update (the rows above the next group's band) runs on the caller's
+  // stream `st` beside the next group's solves.  W and sY alternate between two sets by
+  // group; the next group's first decision uses the recorded bound nYb instead of the
+  // maximum the bulk update is still computing.
+  // (lookahead = 1, the default, is automatic: on for m >= 4096 unless a panel norm exceeds
+  // 2^64 -- then the first decisions of the groups would likely have to scale on the bound
+  // and the call would be recomputed; 2 forces it, 0 disables it)
+  const bool la = can_fuse && (c->lookahead == 2 || (c->lookahead == 1 && m >= 4096 && panel_max <= 0x1p64));
+  cudaStream_t ms = st;
+  int* sY_set[2] = {P.sY, P.sY};
+  if (la) {
+    if (!c->hi) {
+      int lo_p, hi_p;
+      CK(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+      CK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi_p));
+      CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+    }
+    if ((int)c->ev_la.size() < 2 * M + 2) {
+      for (cudaEvent_t e : c->ev_la) cudaEventDestroy(e);
+      c->ev_la.assign(2 * (size_t)M + 2, nullptr);
+      for (auto& e : c->ev_la) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (int k = 0; k < fusion; ++k) CK(c->Wy[k].ensure(c->W.cap));
+    CK(c->sYb.ensure(sizeof(int) * (size_t)n));
+    sY_set[1] = c->sYb.as<int>();
+    ms = c->hi;
+    CK(cudaEventRecord(c->ev_in, st));
+    CK(cudaStreamWaitEvent(ms, c->ev_in, 0));
+  }
+  int n_la_ev = 0;
+  int gpar = 0;                      // W / sY set of the current group (lookahead)
+  bool prev_bound = false;           // the previous group recorded nYb (lookahead)
+  cudaEvent_t ev_rest = nullptr;     // the bulk update of the previous group (lookahead)
   int nyb = (M - 1) & 1;   // nY buffer holding the pending max for the next decision
   static const bool dbg_sync = getenv("ZZ_DEBUG_SYNC") != nullptr;
   auto dbg = [&](const char* what, int I) -> int {
@@ -487,9 +543,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   auto panel_ready = [&](int I) -> int {
     if (!hs) return 0;
     // panel I has arrived: its eigenvalue pairs and column-panel norms
-    CK(cudaStreamWaitEvent(st, (*hs->ev)[I], 0));
-    CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, st));
-    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, st, I, 1));
+    CK(cudaStreamWaitEvent(ms, (*hs->ev)[I], 0));
+    CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, ms));
+    CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, ms, I, 1));
     launches += 2;
     return 0;
   };
@@ -523,6 +579,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.S = Su; d2.lds = ldsu; d2.T = Tu; d2.ldt = ldtu;
       d2.X = X; d2.ldx = ldx;
       d2.P = P;
+      d2.P.sY = sY_set[gpar];
+      static const int la_pack = getenv("ZZ_LA_PACK") ? atoi(getenv("ZZ_LA_PACK")) : 1;
+      d2.pack = la && la_pack;
       d2.nY_in = dp.nY_in;
       d2.Wout = Wout;
       d2.grp_slot = -1;
@@ -540,21 +599,23 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
           d2.prev_W[k] = fuse_from->prev_W[k];
         }
         d2.zero_pend_end = fuse_from->zero_pend_end;
+        d2.use_bound = fuse_from->use_bound;
+        d2.record_bound = fuse_from->record_bound;
         if (d2.fused == 2) d2.nY_in = d2.band_in;
       }
-      CK(launch_diag3(d2, st));
+      CK(launch_diag3(d2, ms));
     } else {
-      CK(launch_diag(dp, st));
+      CK(launch_diag(dp, ms));
     }
     launches++;
     return dbg(fuse_from && fuse_from->fused ? "diag (fused)" : "diag", I);
   };
-  auto update = [&](UpdParams up, int n_m) -> int {
+  auto update = [&](UpdParams up, int n_m, cudaStream_t us) -> int {
     const int n_n = ceil_div(n_sel, kBN) - up.ntile0;
-    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], st));
-    CK(launch_update(&tmS, &tmT, up, n_m, n_n, st));
+    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], us));
+    CK(launch_update(&tmS, &tmT, up, n_m, n_n, us));
     if (int r = dbg(up.nxs ? "fused update" : (up.row_lo ? "thin update" : "update"), up.t0 / std::max(mb, 1))) return r;
-    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], st));
+    if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], us));
     n_upd++;
     launches++;
     return 0;
@@ -572,7 +633,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     up.ntile0 = cs[I] / kBN;
     up.X = X; up.ldx = ldx;
     up.W = P.W;
-    up.sY = P.sY;
+    up.sY = sY_set[gpar];
     up.nY_out = P.nY + (size_t)(1 - nyb) * n;
     up.vec = vec;
     return up;
@@ -602,6 +663,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       double* Wg[kMaxGroup];
       Wg[0] = P.W;
       for (int k = 1; k < len; ++k) Wg[k] = c->Wx[k - 1].as<double>();
+      if (la && gpar == 1)
+        for (int k = 0; k < len; ++k) Wg[k] = c->Wy[k].as<double>();
       for (int sgi = 0; sgi < len; ++sgi) {
         const int X = I - sgi;
         if (sgi > 0 && (r = panel_ready(X))) return r;
@@ -611,6 +674,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
           o.fused = 0;
           o.grp_slot = 0;
           o.n_band_reset = len - 2;
+          o.use_bound = la && prev_bound;
+          if (la && !prev_bound && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
         } else if (sgi < len - 1) {
           o.fused = 2;
           o.grp_slot = sgi;
@@ -626,6 +691,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
             o.prev_W[k] = Wg[k];
           }
           o.zero_pend_end = cs[I + 1];       // tips of the group start from zero pending rows
+          o.record_bound = la;
+          // the decision needs the pending maximum of the rows above tile L (the bulk update
+          // of the previous group)
+          if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
         }
         if ((r = diag(X, Wg[sgi], &o))) return r;
         if (sgi < len - 1) {
@@ -638,7 +707,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
           } else {
             th.max_row = 0;
           }
-          if ((r = update(th, ceil_div(ts[X] - (ts[L] & ~1), kBM)))) return r;
+          if ((r = update(th, ceil_div(ts[X] - (ts[L] & ~1), kBM), ms))) return r;
         }
       }
       UpdParams fu = base_up(L);
@@ -651,12 +720,46 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
         fu.xnks[e] = nks_of(X);
         fu.xW[e] = Wg[I - X];
       }
-      if ((r = update(fu, ceil_div(ts[L], kBM)))) return r;
+      // the next group's band: its tiles L-1 .. L-len_next (the grouping rule of this loop)
+      int len_next = 0;
+      if (la && L - 1 >= 1) {
+        const int In = L - 1;
+        len_next = fusion - (M - 1 - In) % fusion;
+        while (len_next > 1 && In - (len_next - 1) < 1) --len_next;
+      }
+      if (la && len_next >= 1 && ts[L - len_next] > 0) {
+        const int rb = ts[L - len_next];        // rows [rb, ts[L]): the next group's band
+        UpdParams fb = fu;                    // the band first, on the chain's stream
+        fb.row_lo = rb;
+        fb.max_row = 0;
+        if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
+        cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
+        CK(cudaEventRecord(ev_dec, ms));
+        CK(cudaStreamWaitEvent(st, ev_dec, 0));
+        UpdParams fr = fu;                    // the bulk on the caller's stream
+        fr.rows = rb;
+        fr.max_row = rb;
+        if ((r = update(fr, ceil_div(rb, kBM), st))) return r;
+        ev_rest = c->ev_la[n_la_ev++];
+        CK(cudaEventRecord(ev_rest, st));
+        prev_bound = true;
+      } else {
+        if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+        if ((r = update(fu, ceil_div(ts[L], kBM), ms))) return r;
+        ev_rest = nullptr;
+        prev_bound = false;
+      }
       nyb = 1 - nyb;
+      gpar ^= (la ? 1 : 0);
       ++n_fused;
       I -= len;
       continue;
     }
+    if (la && ev_rest) {               // a single step takes the measured maximum
+      CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+      ev_rest = nullptr;
+    }
+    prev_bound = false;
     if ((r = diag(I, P.W, nullptr))) return r;
     if (I > 0) {
       UpdParams up = base_up(I);
@@ -666,10 +769,14 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
         up.Apk = c->Apk.as<double>();
         launches++;
       }
-      if ((r = update(up, ceil_div(ts[I], kBM)))) return r;
+      if ((r = update(up, ceil_div(ts[I], kBM), ms))) return r;
       nyb = 1 - nyb;
     }
     --I;
+  }
+  if (la) {                            // join the chain's stream back into the caller's
+    CK(cudaEventRecord(c->ev_out, ms));
+    CK(cudaStreamWaitEvent(st, c->ev_out, 0));
   }
   CK(cudaEventRecord(c->e2, st));
   // ---- a7 consistency and normalisation ----
@@ -700,20 +807,30 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     if (bS + mdS > 0x1p1020 || bT + mdT > 0x1p1020)
       return tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, cse, nullptr);
   }
+  if (la && stat[6]) {
+    // a group's first decision on the recorded bound would have scaled where the measured
+    // maximum may not: recompute without lookahead (bitwise the plain schedule's result)
+    const int saved = c->lookahead;
+    c->lookahead = 0;
+    const int rr = tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, cse, nullptr);
+    c->lookahead = saved;
+    c->info.lookahead_redo = 1;
+    return rr;
+  }
   info.n_scaled = stat[4];
   info.min_exp = stat[5];
   info.update_launches = n_upd;
   info.fused_pairs = n_fused;
   info.total_launches = launches;
-  float ms;
-  cudaEventElapsedTime(&ms, c->e0, c->e1); info.ms_setup = ms;
-  cudaEventElapsedTime(&ms, c->e1, c->e2); info.ms_steps = ms;
-  cudaEventElapsedTime(&ms, c->e2, c->e3); info.ms_normalize = ms;
+  float el;
+  cudaEventElapsedTime(&el, c->e0, c->e1); info.ms_setup = el;
+  cudaEventElapsedTime(&el, c->e1, c->e2); info.ms_steps = el;
+  cudaEventElapsedTime(&el, c->e2, c->e3); info.ms_normalize = el;
   if (c->timing) {
     double tot = 0;
     for (int u = 0; u < n_upd; ++u) {
-      cudaEventElapsedTime(&ms, c->ev[2 * u], c->ev[2 * u + 1]);
-      tot += ms;
+      cudaEventElapsedTime(&el, c->ev[2 * u], c->ev[2 * u + 1]);
+      tot += el;
     }
     info.ms_update = tot;
   }
@@ -841,6 +958,13 @@ int zz_set_fusion(int k) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (k < 1 || k > kMaxGroup) return -1;
   g_ctx->fusion = k;
+  return 0;
+}
+
+int zz_set_lookahead(int mode) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (mode < 0 || mode > 2) return -1;
+  g_ctx->lookahead = mode;
   return 0;
 }
 

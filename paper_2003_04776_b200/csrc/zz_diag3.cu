@@ -559,6 +559,10 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         P.sY[c] = ef - e_p;
         P.e_pend[c] = ef;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
+        // lookahead: an upper bound of |pending| after this group's update, at exponent ef
+        // (2^(ef-g) (y^ + tau x^), with a margin for the rounding of the sum and the update)
+        if (p.record_bound)
+          P.nYb[c] = scale2k(__dmul_rn(__dadd_rn(yh, __dmul_rn(tau, xh)), 1.0 + 0x1p-40), ef - g0);
       }
       // each earlier W of this column brought to ef (rare), or zero where the column was not
       // active at that step (stale entries)
@@ -586,14 +590,21 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       // it only, whose maximum the previous thin update left in band buffer nY_in; the
       // exponent e_p of the rows above the group stays in e_prev for the last step)
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
-      double nyv = tip ? 0.0 : __longlong_as_double((long long)nyi[c0]);
-      if (PAIR && !tip) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
+      double nyv = 0.0;
+      if (!tip) {
+        // (lookahead: the first step of a group takes the previous group's recorded bound)
+        nyv = p.use_bound ? P.nYb[c0] : __longlong_as_double((long long)nyi[c0]);
+        if (PAIR) nyv = dmaxd(nyv, p.use_bound ? P.nYb[c0 + 1] : __longlong_as_double((long long)nyi[c0 + 1]));
+      }
       const int g0 = min(ep, es);
       const double yh = scale2k(nyv, g0 - ep), xh = scale2k(lm, g0 - es);
       const double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
       const int en = g0 + protect_update(yh, tau, xh);
       sx = en - es;
       if (t == 0) {
+        // lookahead: a shift taken on the recorded bound rather than the measured maximum may
+        // over-scale; flag it, and the call is recomputed without lookahead (zz_api.cu)
+        if (p.use_bound && en < g0) atomicOr(&P.status[6], 1);
         P.sY[c] = en - ep;
         if (p.fused != 2) P.e_prev[c] = ep;   // the pending exponent before this step (read by a fused J/K)
         P.e_pend[c] = en;
@@ -753,15 +764,17 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
   if (p.nt > kDiag2MaxNT) return cudaErrorInvalidValue;
   const size_t smem = smem3(p.nt);
   cudaError_t e;
+  // pack: as few CTAs as the tasks need (one task per warp), leaving the other SMs to a
+  // concurrent update (lookahead); otherwise one task per CTA first (lowest latency alone)
   if (p.nt <= 64) {
     constexpr int nw = W3<8>::n;
-    const int grid = tasks < g_sms3 ? tasks : g_sms3;
+    const int grid = p.pack ? std::min(g_sms3, (tasks + nw - 1) / nw) : (tasks < g_sms3 ? tasks : g_sms3);
     e = cudaFuncSetAttribute(k_diag3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_diag3<8><<<grid, nw * 32, smem, st>>>(p);
   } else {
     constexpr int nw = W3<16>::n;
-    const int grid = tasks < g_sms3 ? tasks : g_sms3;
+    const int grid = p.pack ? std::min(g_sms3, (tasks + nw - 1) / nw) : (tasks < g_sms3 ? tasks : g_sms3);
     e = cudaFuncSetAttribute(k_diag3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_diag3<16><<<grid, nw * 32, smem, st>>>(p);

@@ -79,6 +79,7 @@ struct DevPlan {
   int* sY;            // per column: exponent shift of the pending rows at this step
   int* e_prev;        // per column: pending exponent before a group's first decision
   int* e_grp;         // (kMaxGroup - 1) x n_sel: exponent of each earlier step's W in a group
+  double* nYb;        // per column: upper bound of |pending| after a group's update (lookahead)
   unsigned long long* nY;   // kMaxGroup x n_sel: max |pending| (double bits), 2 alternating + band buffers
   int* e_seg;         // M x n_sel: exponent of each solved segment
   double* nrm_seg;    // M x n_sel: max(|Re|,|Im|) of the segment
@@ -168,6 +169,10 @@ struct Diag2Params {
   int prev_I[kMaxGroup - 1], prev_cs[kMaxGroup - 1], prev_nks[kMaxGroup - 1];
   double* prev_W[kMaxGroup - 1];
   int zero_pend_end;       // columns < zero_pend_end (tips of the group) have no pending rows
+  // lookahead: a group's first step takes the pending bound nYb recorded by the previous
+  // group's last step (use_bound) instead of the measured maximum; the last step records it
+  int use_bound, record_bound;
+  int pack;                // launch as few CTAs as the tasks need (lookahead)
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)

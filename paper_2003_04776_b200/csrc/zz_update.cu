@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // MODE 1 (two-step fused update): a second K segment; MODE 2 (thin update): first row row_lo
-  constexpr bool SEG2 = MODE == 1;
+  constexpr bool SEG2 = MODE == 1 || MODE == 3;   // MODE 3: segments and a first row (lookahead band)
   // K chunks: segment 0 (t0, nks, W), then the group's further segments (MODE 1)
   const int nkca = 2 * p.nks;
   int nkc = nkca;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
     for (int e = 0; e < kMaxGroup - 1; ++e) nkc += (e < p.nxs) ? 2 * p.xnks[e] : 0;
   }
   const int n_ntl = n_tiles / n_mtiles;
-  const int row_lo = (MODE == 2) ? p.row_lo : 0;
+  const int row_lo = (MODE >= 2) ? p.row_lo : 0;   // MODE 3: the lookahead's band part
   const int mbase = row_lo & ~1;                         // 16-byte aligned first row pair
   // W is stored per 64-column block: [ntile64][kc][BK/4][64][4] (per segment)
   const long long wtile = (long long)nkca * (kBN * kBK);
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(UT<WN>::THREADS, UT<WN>::MINB)
         const bool both = cvalid && (i0 + 1 < p.rows) && (i0 >= row_lo);
         st2h(xc + i0, v0, v1, both, pol_s);
         st1h(xc + i0, v0, cvalid && i0 + 1 == p.rows && i0 >= row_lo, pol_s);
-        if (MODE == 2) st1h(xc + i0 + 1, v1, cvalid && i0 + 1 == row_lo && i0 + 1 < p.rows, pol_s);
+        if (MODE >= 2) st1h(xc + i0 + 1, v1, cvalid && i0 + 1 == row_lo && i0 + 1 < p.rows, pol_s);
         if (i0 < p.max_row) cm = fmax(cm, fabs(v0));
         if (i0 + 1 < p.max_row) cm = fmax(cm, fabs(v1));
       }
@@ -610,6 +610,7 @@ static cudaError_t launch_update_impl(const CUtensorMap* tmS, const CUtensorMap*
                                       int n_mtiles, int n_ntiles, cudaStream_t st, int ver, int persist) {
   // the template kernels move C in 16-byte pairs: X 16-byte aligned with an even ldx
   if (ver == 2 && p.vec) {
+    if (p.nxs > 0 && p.row_lo > 0) return launch_t<2, 8, 3>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
     if (p.nxs > 0) return launch_t<2, 8, 1>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
     if (p.row_lo > 0) return launch_t<2, 8, 2>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);
     return launch_t<2, 8>(tmS, tmT, p, n_mtiles, n_ntiles, st, persist);

@@ -582,3 +582,47 @@ def test_fusion_modes_stress(zz, fusion):
         assert w <= 10 * S.shape[0] * U, w
     finally:
         zz.set_fusion(4)
+
+
+
+# ---- lookahead schedule (zz_set_lookahead) ----
+
+def test_lookahead_bitwise_and_parity(zz):
+    # m = 4096: the automatic mode turns it on; results are bitwise those of the plain
+    # schedule (no scaling triggers) and within the parity tolerance of the oracle
+    S, T, _ = gen.config("C3", seed=2, m=4096, n2=614)
+    try:
+        zz.set_lookahead(0)
+        X0, e0, _ = solve(zz, S, T, mb=128)
+        zz.set_lookahead(1)
+        X1, e1, info = solve(zz, S, T, mb=128)
+        assert info["lookahead_redo"] == 0
+        assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
+        check_against_oracle(S, T, X1, e1)
+        # host path with lookahead: bitwise the device path
+        Xh, eh, _ = _host_solve(zz, S, T, 128)
+        assert np.array_equal(Xh, X0) and np.array_equal(eh, e0)
+    finally:
+        zz.set_lookahead(1)
+
+
+def test_lookahead_forced_on_stress_recomputes(zz):
+    # forced on a pencil that scales: the bound-based first decisions would over-scale, the
+    # call is recomputed without lookahead -- bitwise the plain schedule
+    S, T = _stress(2000, 2)
+    try:
+        zz.set_lookahead(0)
+        X0, e0, _ = solve(zz, S, T, mb=64)
+        zz.set_lookahead(2)
+        X1, e1, info = solve(zz, S, T, mb=64)
+        assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
+        assert info["lookahead_redo"] == 1
+        # a small well-scaled pencil forced on: no redo, bitwise
+        S2, T2, _ = gen.config("C2", seed=1)
+        zz.set_lookahead(0)
+        Y0, f0, _ = solve(zz, S2, T2, mb=64)
+        zz.set_lookahead(2)
+        Y1, f1, info2 = solve(zz, S2, T2, mb=64)
+        assert info2["lookahead_redo"] == 0 and np.array_equal(Y0, Y1) and np.array_equal(f0, f1)
+    finally:
+        zz.set_lookahead(1)

@@ -68,6 +68,7 @@ def test_no_context_and_bad_args():
     assert lib.zz_tgevc_left(3, p, 3, p, 3, None, p, 3, None) == -103
     assert lib.zz_set_tile(64) == -103
     assert lib.zz_set_fusion(3) == -103
+    assert lib.zz_set_lookahead(1) == -103
     assert lib.zz_status_string(-105).decode().startswith("overlapping")
     assert lib.zz_status_string(3).decode().startswith("a 2x2")
 
