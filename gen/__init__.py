@@ -85,3 +85,23 @@ def orthogonal(m, seed=0):
     d = np.sign(np.diag(R))
     d[d == 0] = 1.0
     return np.asfortranarray(Q * d)
+
+
+def complex_pencil(m, var_off=None, seed=0, stress=False):
+    """Seeded complex Schur pencil (S, T), complex128 column-major m x m, T with a real
+    positive diagonal (the ZTGEVC input form).  Built from two real upper-triangular pencils
+    of generate() (n2 = 0, off-diagonals N(0, var_off)): S = S1 + i S2, T = T1 + i triu(T2, 1),
+    so Re(lambda_j) = S1_jj / T1_jj keeps generate()'s per-eigenvalue separation.
+    stress=True multiplies the strictly-upper entries of S by 1e150 in alternate rows so that
+    the unprotected substitution overflows (the robust-scaling workload)."""
+    if var_off is None:
+        var_off = min(1.0, 1.0 / max(m, 1))
+    S1, T1, _ = generate(m, 0, var_off, seed=seed)
+    S2, T2, _ = generate(m, 0, var_off, seed=seed + 7777)
+    S = np.asfortranarray(S1 + 1j * S2)
+    T = np.asfortranarray(T1 + 1j * np.triu(T2, 1))
+    if stress:
+        U = np.triu(np.ones((m, m), dtype=bool), 1)
+        U[1::2, :] = False
+        S[U] *= 1e150
+    return S, T

@@ -15,10 +15,10 @@ _lib = None
 
 
 def build(force=False):
-    src = os.path.join(_HERE, "zz_oracle.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, f) for f in ("zz_oracle.c", "zz_oracle_z.c")]
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(s) for s in srcs):
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-o", _SO, src, "-lm"])
+                               "-o", _SO] + srcs + ["-lm"])
     return _SO
 
 
@@ -42,6 +42,10 @@ def _load():
         lib.zzo_count_columns.argtypes = [ci, vp, ci, vp]
         lib.zzo_flops.restype = cd
         lib.zzo_flops.argtypes = [ci, vp, ci, vp]
+        lib.zzo_zeig.restype = ci
+        lib.zzo_zeig.argtypes = [ci, vp, ci, vp, ci, vp, vp, vp, vp]
+        lib.zzo_ztgevc.restype = ci
+        lib.zzo_ztgevc.argtypes = [ci, vp, ci, vp, ci, vp, vp, ci, vp, vp, ci, ci]
         _lib = lib
     return _lib
 
@@ -198,3 +202,38 @@ def tgevc_left(S, T, select=None):
         Y[:, c] = sg * Xf[::-1, src]
         e[c] = r["e"][src]
     return dict(Y=Y, e=e, pairs=r["pairs"][::-1].copy(), status=0)
+
+
+def _z(A):
+    A = np.asarray(A, dtype=np.complex128)
+    if A.ndim != 2 or not A.flags.f_contiguous:
+        A = np.asfortranarray(A, dtype=np.complex128)
+    return A
+
+
+def zeig(S, T):
+    """normalised (alpha, beta) per row of a complex Schur pencil (oracle/zz_oracle_z.c R18):
+    returns (alpha complex array, beta, kind, status)"""
+    S, T = _z(S), _z(T)
+    m = S.shape[0]
+    a, b, be = (np.zeros(max(m, 1)) for _ in range(3))
+    kd = np.zeros(max(m, 1), np.int32)
+    st = _load().zzo_zeig(m, S.ctypes.data, max(m, 1), T.ctypes.data, max(m, 1), a.ctypes.data,
+                          b.ctypes.data, be.ctypes.data, kd.ctypes.data)
+    return (a + 1j * b)[:m], be[:m], kd[:m], st
+
+
+def ztgevc(S, T, select=None, protect=True, nthreads=0):
+    """Robust column-by-column eigenvectors of a complex Schur pencil (ZTGEVC analogue,
+    oracle/zz_oracle_z.c).  Returns dict(X complex m x n_sel, e, stats, status)."""
+    S, T = _z(S), _z(T)
+    m = S.shape[0]
+    sel = _sel(select, m)
+    n = m if sel is None else int(np.count_nonzero(sel))
+    X = np.zeros((m, max(n, 1)), dtype=np.complex128, order="F")
+    e = np.zeros(max(n, 1), np.int32)
+    stats = np.zeros(3, np.int32)
+    st = _load().zzo_ztgevc(m, S.ctypes.data, max(m, 1), T.ctypes.data, max(m, 1),
+                            None if sel is None else sel.ctypes.data, X.ctypes.data, max(m, 1),
+                            e.ctypes.data, stats.ctypes.data, 1 if protect else 0, nthreads)
+    return dict(X=X[:, :n], e=e[:n], stats=stats, status=st)

@@ -89,3 +89,27 @@ def dtgevc_left(S, T, select=None):
               T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), m, VR.ctypes.data_as(vp), 1, m,
               ctypes.byref(mo))
     return info, VL[:, :mo.value]
+
+
+def ztgevc(S, T, select=None):
+    """LAPACK ZTGEVC right eigenvectors (HOWMNY='A' or 'S'); returns (info, VR complex)."""
+    lib = ctypes.CDLL(_paths()[0])
+    f = lib.scipy_LAPACKE_ztgevc
+    f.restype = ctypes.c_int
+    S = np.asfortranarray(S, dtype=np.complex128)
+    T = np.asfortranarray(T, dtype=np.complex128)
+    m = S.shape[0]
+    VR = np.zeros((m, max(m, 1)), dtype=np.complex128, order="F")
+    VL = np.zeros((1, 1), dtype=np.complex128)
+    mo = ctypes.c_int(0)
+    if select is None:
+        how, sel = b"A", None
+    else:
+        how = b"S"
+        sel = np.ascontiguousarray(np.asarray(select, dtype=np.int32))
+    vp = ctypes.c_void_p
+    info = f(102, ctypes.c_char(b"R"), ctypes.c_char(how),
+             None if sel is None else sel.ctypes.data_as(vp), m, S.ctypes.data_as(vp), m,
+             T.ctypes.data_as(vp), m, VL.ctypes.data_as(vp), 1, VR.ctypes.data_as(vp), m, m,
+             ctypes.byref(mo))
+    return info, VR[:, :mo.value]
