@@ -26,6 +26,7 @@
  *  -104   non-finite entry in a diagonal block of S or T
  *  -105   overlapping 2x2 blocks (two consecutive nonzero subdiagonal entries of S)
  *  -106   unsupported tile size
+ *  -107   zz_ztgevc: a diagonal entry of T is not real
  * There is no CPU fallback: without a CUDA device every call returns -100 or -103.
  *
  * Threading.  One context per host thread (thread-local), bound to one device.  Calls on
@@ -47,6 +48,7 @@ extern "C" {
 #define ZZ_ERR_NONFINITE (-104)
 #define ZZ_ERR_OVERLAP (-105)
 #define ZZ_ERR_TILE (-106)
+#define ZZ_ERR_CPLXDIAG (-107)
 
 /* Statistics of the last zz_tgevc call of this thread's context. */
 typedef struct zz_info {
@@ -171,6 +173,32 @@ int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, con
  * refers to rows of S.  Ownership and errors as zz_tgevc. */
 int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, const int* select,
                   double* Y, int ldy, int* col_scale_exp);
+
+/* zz_ztgevc: selected right eigenvectors of a COMPLEX pencil in generalized complex Schur
+ * form (the ZTGEVC analogue; PAPER.md:333 names complex pencils as the next step): S and T
+ * upper triangular, T with a real diagonal.  For (alpha, beta) = (S_jj, T_jj) the eigenvector
+ * z solves (beta S - alpha T) z = 0 with z_i = 0 for i > j (Lemma 1, all
+ * blocks 1x1), computed by the robust blocked substitution (Algorithms 1-3)
+ * with complex entries (readings R18-R21).
+ *   m              order (m >= 0)                                                [arg 1]
+ *   S, lds         DEVICE, m x m complex column-major, INTERLEAVED (re, im) doubles
+ *                  (LAPACK COMPLEX*16 layout); lds in complex elements; never written.
+ *                  The strictly lower part is never read.                      [args 2,3]
+ *   T, ldt         DEVICE, as S; Im T_jj must be 0 (else -107)                  [args 4,5]
+ *   select         HOST int[m] or NULL (all); select[j] != 0 picks eigenvalue j; output
+ *                  columns in increasing j.                                      [arg 6]
+ *   X, ldx         DEVICE, m x n_sel complex interleaved, ldx (complex elements) >= m;
+ *                  written completely: z_i = 0 for i > j, normalised as ZTGEVC does,
+ *                  max_i (|Re z_i| + |Im z_i|) = 1, from a real positive z_j before
+ *                  normalisation; alpha = beta = 0 gives e_j.                  [args 7,8]
+ *   col_scale_exp  DEVICE int32[n_sel] or NULL: exponents as zz_tgevc.            [arg 9]
+ * Tiles of zz_set_tile() rows when 16..64, else 64.  The update of each step is one complex
+ * contraction of K = 2 x tile (cuBLAS ZGEMM over a copy of the S and T panels); the solves,
+ * scaling decisions, panel copies and normalisation are this library's kernels.  The call
+ * allocates its workspace stream-ordered (cudaMallocAsync) and returns after the stream has
+ * completed.  Status codes as zz_tgevc (-104 non-finite diagonal entry, -107). */
+int zz_ztgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,
+              double* X, int ldx, int* col_scale_exp);
 
 /* Number of output columns zz_tgevc would produce for (S, select) with S on the HOST
  * (pairs count 2).  Returns n_sel >= 0, -105, or -i for a bad argument.  Host-only. */

@@ -25,9 +25,10 @@ STATUS = {
     -104: "non-finite entry in a diagonal block",
     -105: "overlapping 2x2 blocks",
     -106: "unsupported tile size",
+    -107: "a diagonal entry of T is not real (zz_ztgevc)",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left",
+EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left", "zz_ztgevc",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -84,6 +85,7 @@ def load(build_if_missing=True):
         "zz_tgevc_host": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_tgevc_back": ([ci, vp, ci, vp, ci, vp, vp, ci, vp, ci, vp], ci),
         "zz_tgevc_left": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
+        "zz_ztgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
         "zz_count_columns": ([ci, vp, ci, vp], ci),
         "zz_partition": ([ci, vp, ci, vp], ci),
         "zz_last_info": ([ctypes.POINTER(Info)], ci),
@@ -237,6 +239,38 @@ def tgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None, n_sel=None
                      X.data_ptr() if n_sel > 0 else ctypes.c_void_p(1), ldx,
                      col_scale_exp.data_ptr() if n_sel > 0 else None)
     _check(r, "zz_tgevc")
+    return X, col_scale_exp
+
+
+def ztgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None):
+    """Selected right eigenvectors of a COMPLEX Schur pencil (ZTGEVC analogue, include/zz.h
+    zz_ztgevc): S, T complex128 CUDA tensors, m x m, column-major, Im T_jj = 0.  Returns
+    (X, col_scale_exp), X an m x n_sel complex128 column-major CUDA tensor."""
+    import torch
+    lib = load()
+    m = S.shape[0]
+    if not (S.is_cuda and T.is_cuda):
+        raise ValueError("S and T must be CUDA tensors (no CPU fallback)")
+    if S.dtype != torch.complex128 or T.dtype != torch.complex128:
+        raise ValueError("S and T must be complex128")
+    dev = S.device.index
+    if dev not in _inited:
+        init(dev)
+    lds = _ld_colmajor(S, m, "S")
+    ldt = _ld_colmajor(T, m, "T")
+    sel = _sel_array(select, m)
+    n_sel = m if sel is None else int((sel != 0).sum())
+    if X is None:
+        X = torch.empty((max(n_sel, 1), m), dtype=torch.complex128, device=S.device).t()[:, :n_sel]
+    ldx = _ld_colmajor(X, m, "X") if n_sel > 0 else max(m, 1)
+    if col_scale_exp is None:
+        col_scale_exp = torch.empty(max(n_sel, 1), dtype=torch.int32, device=S.device)[:n_sel]
+    st = stream if stream is not None else torch.cuda.current_stream(S.device)
+    _check(lib.zz_set_stream(ctypes.c_void_p(st.cuda_stream)), "zz_set_stream")
+    r = lib.zz_ztgevc(m, S.data_ptr(), lds, T.data_ptr(), ldt, None if sel is None else sel.ctypes.data,
+                      X.data_ptr() if n_sel > 0 else ctypes.c_void_p(1), ldx,
+                      col_scale_exp.data_ptr() if n_sel > 0 else None)
+    _check(r, "zz_ztgevc")
     return X, col_scale_exp
 
 

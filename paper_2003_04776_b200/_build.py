@@ -8,7 +8,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libzz.so")
-SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu", "zz_back.cu", "zz_left.cu"]
+SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu", "zz_back.cu", "zz_left.cu", "zz_complex.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

@@ -922,6 +922,22 @@ int check_args(int m, const double* S, int lds, const double* T, int ldt, double
 
 }  // namespace
 
+// Context access for the complex-pencil path (zz_complex.cu): binds the device, creates the
+// cuBLAS handle on the context's stream, and hands out the stream, tile and info record.
+int ctx_acquire(cudaStream_t* st, cublasHandle_t* blas, int* mb, zz_info_t** info) {
+  Context* c = g_ctx;
+  if (!c) return ZZ_ERR_NOCTX;
+  if (cudaSetDevice(c->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  if (cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
+  *st = c->stream;
+  *blas = c->blas;
+  *mb = c->mb;
+  *info = &c->info;
+  return 0;
+}
+
 extern "C" {
 
 int zz_init(int device) {
@@ -1140,6 +1156,7 @@ const char* zz_status_string(int s) {
     case ZZ_ERR_NONFINITE: return "non-finite entry in a diagonal block of S or T";
     case ZZ_ERR_OVERLAP: return "overlapping 2x2 blocks (two consecutive nonzero subdiagonals)";
     case ZZ_ERR_TILE: return "unsupported tile size";
+    case ZZ_ERR_CPLXDIAG: return "a diagonal entry of T is not real (zz_ztgevc)";
     default: return (s >= -9) ? "invalid argument" : "unknown status";
   }
 }

@@ -69,6 +69,11 @@ def test_no_context_and_bad_args():
     assert lib.zz_set_tile(64) == -103
     assert lib.zz_set_fusion(3) == -103
     assert lib.zz_set_lookahead(1) == -103
+    assert lib.zz_ztgevc(-1, p, 3, p, 3, None, p, 3, None) == -1
+    assert lib.zz_ztgevc(3, p, 3, p, 2, None, p, 3, None) == -5
+    assert lib.zz_ztgevc(3, p, 3, p, 3, None, p, 2, None) == -8
+    assert lib.zz_ztgevc(3, p, 3, p, 3, None, p, 3, None) == -103
+    assert lib.zz_status_string(-107).decode().startswith("a diagonal entry of T")
     assert lib.zz_status_string(-105).decode().startswith("overlapping")
     assert lib.zz_status_string(3).decode().startswith("a 2x2")
 
