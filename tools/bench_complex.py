@@ -1,0 +1,70 @@
+"""Timing of zz_ztgevc (complex pencils) on one GPU.
+
+python tools/bench_complex.py --m 10000 --steps 3 --warmup 2
+Prints one JSON line: seconds per call (CUDA events on the launching stream, inputs
+resident in HBM, larger than L2 at m >= 4000), nominal flops F_z = sum_j 8 j (j + 1)
+(every (i, k) pair i < k <= j of column j costs two complex multiply-adds = 16 flop), the
+FP64 fraction against the DMMA peak, and a sampled parity check against the oracle."""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import gen  # noqa: E402
+import paper_2003_04776_b200 as zz  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--m", type=int, default=10000)
+ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--no-check", action="store_true")
+args = ap.parse_args()
+
+m = args.m
+t0 = time.time()
+S, T = gen.complex_pencil(m, seed=args.seed)
+tgen = time.time() - t0
+zz.init(0)
+zz.set_tile(args.tile)
+Sd = torch.from_numpy(S).cuda().t().contiguous().t()
+Td = torch.from_numpy(T).cuda().t().contiguous().t()
+st = torch.cuda.current_stream()
+X, E = zz.ztgevc(Sd, Td)
+for _ in range(args.warmup):
+    zz.ztgevc(Sd, Td, X=X, col_scale_exp=E)
+torch.cuda.synchronize()
+e0 = torch.cuda.Event(enable_timing=True)
+e1 = torch.cuda.Event(enable_timing=True)
+e0.record(st)
+for _ in range(args.steps):
+    zz.ztgevc(Sd, Td, X=X, col_scale_exp=E)
+e1.record(st)
+torch.cuda.synchronize()
+sec = e0.elapsed_time(e1) / 1e3 / args.steps
+j = np.arange(m, dtype=np.float64)
+F = float(np.sum(8.0 * j * (j + 1.0)))
+info = zz.last_info()
+out = {"metric": "seconds & FP64 TFLOP/s, all eigenvectors of a complex Schur pencil (zz_ztgevc)",
+       "m": m, "tile": info["mb"], "steps": args.steps, "warmup": args.warmup,
+       "seconds_per_call": sec, "flops_nominal": F, "value": F / sec * 1e-12, "unit": "TFLOP/s",
+       "fraction_of_fp64_peak": F / sec * 1e-12 / 37.0,
+       "peak_source": "DMMA FP64 37.0 TFLOP/s measured (profiles/r01_fp64_peak.json)",
+       "launches_per_call": info["total_launches"], "update_launches": info["update_launches"],
+       "data": "synthetic: gen.complex_pencil (two real generate() pencils, off-diagonals N(0,1/m))",
+       "gen_seconds": tgen}
+if not args.no_check:
+    import oracle
+    cols = sorted(set([0, m // 3, m // 2, m - 2, m - 1]))
+    sel = np.zeros(m, np.int32)
+    sel[cols] = 1
+    ref = oracle.ztgevc(S, T, select=sel)
+    Xh = X[:, cols].cpu().numpy()
+    out["parity_sample"] = {"columns": cols, "max_abs": float(np.abs(Xh - ref["X"]).max()), "tolerance": 1e-10}
+print(json.dumps(out), flush=True)
