@@ -169,6 +169,27 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
       if (lane + 32 <= top) y1 = xc[lane + 32];
     }
     int e = tipc ? 0 : p.e_pend[c];
+    // Off the dependent chain: the pivots of the lane's two rows (R20) and their reciprocals
+    // (Smith's formula for 1/d), the ProtectDivision thresholds, and the bound bw >= max |y|
+    // over the pending in-tile rows (exact at the start).
+    double2 inv0 = make_double2(0.0, 0.0), inv1 = inv0;
+    double td0 = 1.0, td1 = 1.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      if (r <= top) {
+        const double2 s = Ss[r * nt + r];
+        const double t = Ts[r * nt + r].x;
+        double2 d = make_double2(__dsub_rn(__dmul_rn(be, s.x), __dmul_rn(al.x, t)),
+                                 __dsub_rn(__dmul_rn(be, s.y), __dmul_rn(al.y, t)));
+        const double smin = fmax(kU * (be * zabs1(s) + aa * fabs(t)), kSmlnum);
+        if (zabs1(d) < smin) d = make_double2(smin, 0.0);
+        const double2 iv = zdiv(make_double2(1.0, 0.0), d);
+        const double td = 0.5 * fmin(1.0, zabsm(d));
+        if (h == 0) { inv0 = iv; td0 = td; } else { inv1 = iv; td1 = td; }
+      }
+    }
+    double bw = warp_max(fmax(zabsm(y0), zabsm(y1)));
     for (int i = top; i >= 0; --i) {
       const int own = i & 31;
       const bool hi = i >= 32;
@@ -177,38 +198,43 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
         xi = make_double2(1.0, 0.0);
         if (lane == own) { if (hi) y1 = xi; else y0 = xi; }
       } else {
-        const double2 s = Ss[i * nt + i];
-        const double t = Ts[i * nt + i].x;
-        double2 d = make_double2(__dsub_rn(__dmul_rn(be, s.x), __dmul_rn(al.x, t)),
-                                 __dsub_rn(__dmul_rn(be, s.y), __dmul_rn(al.y, t)));
-        const double smin = fmax(kU * (be * zabs1(s) + aa * fabs(t)), kSmlnum);
-        if (zabs1(d) < smin) d = make_double2(smin, 0.0);
-        const double2 yi0 = hi ? y1 : y0;
-        const double2 yi = make_double2(__shfl_sync(0xffffffffu, yi0.x, own), __shfl_sync(0xffffffffu, yi0.y, own));
-        const int k = protect_division(zabsm(yi), 0.5 * fmin(1.0, zabsm(d)));
-        double2 yv = yi;
+        // ProtectDivision in the owner lane, then x_i = y_i * (1/d_i)
+        int k = 0;
+        if (lane == own) k = protect_division(zabsm(hi ? y1 : y0), hi ? td1 : td0);
+        k = __shfl_sync(0xffffffffu, k, own);
         if (k < 0) {
           y0 = zldexp(y0, k);
           y1 = zldexp(y1, k);
-          yv = zldexp(yv, k);
+          bw = ldexp(bw, k);
           e += k;
         }
-        xi = zdiv(yv, d);
-        if (lane == own) { if (hi) y1 = xi; else y0 = xi; }
+        if (lane == own) {
+          if (hi) y1 = zmul(y1, inv1); else y0 = zmul(y0, inv0);
+        }
+        const double2 xo = hi ? y1 : y0;
+        xi = make_double2(__shfl_sync(0xffffffffu, xo.x, own), __shfl_sync(0xffffffffu, xo.y, own));
       }
       if (i == 0) break;
-      // ProtectUpdate of the in-tile rows above (R19 bound)
-      double wm = 0.0;
-      if (lane < i) wm = zabsm(y0);
-      if (lane + 32 < i) wm = fmax(wm, zabsm(y1));
-      wm = warp_max(wm);
+      // ProtectUpdate of the in-tile rows above (R19 bound).  The bound bw
+      // decides first; only when it cannot exclude a scaling is the exact maximum reduced,
+      // so the decision is the one the exact maximum gives.
       const double tb = 2.0 * (be * cS[i] + aa * cT[i]);
-      const int k2 = protect_update(wm, tb, zabsm(xi));
-      if (k2 < 0) {
-        y0 = zldexp(y0, k2);
-        y1 = zldexp(y1, k2);
-        xi = zldexp(xi, k2);
-        e += k2;
+      double ax = zabsm(xi);
+      if (protect_update(bw, tb, ax) < 0) {
+        double wm = 0.0;
+        if (lane < i) wm = zabsm(y0);
+        if (lane + 32 < i) wm = fmax(wm, zabsm(y1));
+        wm = warp_max(wm);
+        const int k2 = protect_update(wm, tb, ax);
+        if (k2 < 0) {
+          y0 = zldexp(y0, k2);
+          y1 = zldexp(y1, k2);
+          xi = zldexp(xi, k2);
+          wm = ldexp(wm, k2);
+          ax = zabsm(xi);
+          e += k2;
+        }
+        bw = wm;
       }
       const double2 u = make_double2(be * xi.x, be * xi.y);   // x D
       const double2 v = zmul(al, xi);                          // x B
@@ -222,6 +248,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
         y1.x = y1.x - (ps.x - pt.x);
         y1.y = y1.y - (ps.y - pt.y);
       }
+      bw = bw + tb * ax;
     }
     if (lane <= top) xc[lane] = y0;
     if (lane + 32 <= top) xc[lane + 32] = y1;
@@ -256,7 +283,11 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     __syncwarp();
     if (lane == 0) {
       p.e_pend[c] = en;
-      p.nYb[c] = ldexp(yh + tau * xh, ed) * (1.0 + 0x1p-40);   // R21: bound, not a measurement
+      // R21: the bound 2^ed (yh + tau xh), not a measurement; tau xh itself may exceed the
+      // range when ed < 0, so that product is formed as protect_update does (scaled by 2^-1023)
+      const double bnd = ed == 0 ? yh + tau * xh
+                                 : ldexp(yh, ed) + ldexp(ldexp(tau, -512) * ldexp(xh, -511), ed + 1023);
+      p.nYb[c] = bnd * (1.0 + 0x1p-40);
     }
     if (sy < 0) {
       double2* yc = p.X + (long long)c * p.ldx;
@@ -429,7 +460,7 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.e_seg = d_eseg + (size_t)I * n;
     p.nrmh_seg = d_nrmh + (size_t)I * n;
     p.B = d_B;
-    const int grid = std::min((n_act + kZWarps - 1) / kZWarps, 2 * nsm);
+    const int grid = std::min((n_act + kZWarps - 1) / kZWarps, nsm);   // one 132 KB CTA per SM
     k_zdiag<<<grid, kZWarps * 32, smem, st>>>(p);
     ++launches;
     ZCK(cudaGetLastError());
