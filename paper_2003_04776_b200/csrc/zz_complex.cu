@@ -48,6 +48,7 @@ struct ZDiagParams {
   int* e_seg;        // row I of the M x n_sel array
   double* nrmh_seg;  // row I
   double2* B;        // 2 nt x n_act, column-major (ld 2 nt)
+  int* sy;           // per column: exponent shift of the pending rows (<= 0)
 };
 
 __device__ __forceinline__ double zabsm(double2 z) { return fmax(fabs(z.x), fabs(z.y)); }
@@ -55,6 +56,18 @@ __device__ __forceinline__ double zabs1(double2 z) { return fabs(z.x) + fabs(z.y
 __device__ __forceinline__ double2 zmul(double2 x, double2 y) {
   return make_double2(__dsub_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y)),
                       __dadd_rn(__dmul_rn(x.x, y.y), __dmul_rn(x.y, y.x)));
+}
+// y - s*u + t*v with fused multiply-adds
+__device__ __forceinline__ double2 zaxpy2(double2 y, double2 s, double2 u, double2 t, double2 v) {
+  double re = fma(-s.x, u.x, y.x);
+  re = fma(s.y, u.y, re);
+  re = fma(t.x, v.x, re);
+  re = fma(-t.y, v.y, re);
+  double im = fma(-s.x, u.y, y.y);
+  im = fma(-s.y, u.x, im);
+  im = fma(t.x, v.y, im);
+  im = fma(t.y, v.x, im);
+  return make_double2(re, im);
 }
 __device__ __forceinline__ double2 zldexp(double2 z, int k) { return make_double2(ldexp(z.x, k), ldexp(z.y, k)); }
 // Smith's division (R20)
@@ -238,16 +251,10 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
       }
       const double2 u = make_double2(be * xi.x, be * xi.y);   // x D
       const double2 v = zmul(al, xi);                          // x B
-      if (lane < i) {
-        const double2 ps = zmul(Ss[i * nt + lane], u), pt = zmul(Ts[i * nt + lane], v);
-        y0.x = y0.x - (ps.x - pt.x);
-        y0.y = y0.y - (ps.y - pt.y);
-      }
-      if (lane + 32 < i) {
-        const double2 ps = zmul(Ss[i * nt + lane + 32], u), pt = zmul(Ts[i * nt + lane + 32], v);
-        y1.x = y1.x - (ps.x - pt.x);
-        y1.y = y1.y - (ps.y - pt.y);
-      }
+      // y_l <- y_l - S_li u + T_li v as 8 fused multiply-adds per row (the oracle rounds each
+      // product: results agree to rounding, R22)
+      if (lane < i) y0 = zaxpy2(y0, Ss[i * nt + lane], u, Ts[i * nt + lane], v);
+      if (lane + 32 < i) y1 = zaxpy2(y1, Ss[i * nt + lane + 32], u, Ts[i * nt + lane + 32], v);
       bw = bw + tb * ax;
     }
     if (lane <= top) xc[lane] = y0;
@@ -289,10 +296,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
                                  : ldexp(yh, ed) + ldexp(ldexp(tau, -512) * ldexp(xh, -511), ed + 1023);
       p.nYb[c] = bnd * (1.0 + 0x1p-40);
     }
-    if (sy < 0) {
-      double2* yc = p.X + (long long)c * p.ldx;
-      for (int i = lane; i < r0; i += 32) yc[i] = zldexp(yc[i], sy);
-    }
+    if (lane == 0) p.sy[c] = sy;   // applied to the pending rows by k_zscale_pending
     double2* Bc = p.B + (long long)w * 2 * nt;
     const double2 x0 = zldexp(y0, sx), x1 = zldexp(y1, sx);
     if (lane < nt) {
@@ -308,6 +312,19 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
       Bc[nt + lane + 32] = z ? make_double2(0.0, 0.0) : make_double2(-q.x, -q.y);
     }
   }
+}
+
+// sigma_Y of Algorithm 3: Y(0:r0, c) <- 2^sy[c] Y(0:r0, c) for the columns whose decision
+// scaled (rare); one warp per active column.  Runs on the update's stream, after the previous
+// step's update has written those rows.
+__global__ void k_zscale_pending(double2* X, long long ldx, int r0, int cs, int n_act, const int* __restrict__ sy) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_act) return;
+  const int c = cs + w;
+  const int k = sy[c];
+  if (k >= 0) return;
+  double2* yc = X + (long long)c * ldx;
+  for (int i = threadIdx.x & 31; i < r0; i += 32) yc[i] = zldexp(yc[i], k);
 }
 
 // (4) consistency and normalisation: e_c = min_I e_seg[I][c]; X <- ldexp(X, e_c - e_seg) / xmax
@@ -403,12 +420,12 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   double2* X = reinterpret_cast<double2*>(X_);
   if (n == 0) return 0;
   // workspace (stream-ordered)
-  size_t off[12], tot = 0;
-  const size_t sz[12] = {sizeof(int) * n, sizeof(double2) * n, sizeof(double) * n, sizeof(int) * n, sizeof(double) * n,
+  size_t off[13], tot = 0;
+  const size_t sz[13] = {sizeof(int) * n, sizeof(double2) * n, sizeof(double) * n, sizeof(int) * n, sizeof(double) * n,
                          sizeof(int) * (size_t)M * n, sizeof(double) * (size_t)M * n, sizeof(double) * m,
-                         sizeof(double) * m, sizeof(double2) * 2 * (size_t)nb * n,
-                         sizeof(double2) * 2 * (size_t)nb * (size_t)m, sizeof(int) * 4};
-  for (int i = 0; i < 12; ++i) { off[i] = tot; tot += align256(sz[i]); }
+                         sizeof(double) * m, sizeof(double2) * 4 * (size_t)nb * n,
+                         sizeof(double2) * 2 * (size_t)nb * (size_t)m, sizeof(int) * 4, sizeof(int) * n};
+  for (int i = 0; i < 13; ++i) { off[i] = tot; tot += align256(sz[i]); }
   ZWork wk;
   ZCK(wk.alloc(tot, st));
   char* base = static_cast<char*>(wk.p);
@@ -424,6 +441,7 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   double2* d_B = reinterpret_cast<double2*>(base + off[9]);
   double2* d_A = reinterpret_cast<double2*>(base + off[10]);
   int* d_status = reinterpret_cast<int*>(base + off[11]);
+  int* d_sy = reinterpret_cast<int*>(base + off[12]);
   int launches = 0;
   ZCK(cudaMemcpyAsync(d_jcol, jcol.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
   const int big = 0x7fffffff;
@@ -446,12 +464,40 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  int cs = n;   // first active column (columns with jcol >= r0)
-  for (int I = M - 1; I >= 0; --I) {
-    const int r0 = I * nb, nt = std::min(nb, m - r0);
-    while (cs > 0 && jcol[cs - 1] >= r0) --cs;
-    const int n_act = n - cs;
-    if (n_act == 0) continue;
+  // first active column of each step (columns with jcol >= r0); the active set only grows as
+  // I decreases, so the empty steps are the top ones
+  std::vector<int> csI(M);
+  {
+    int cs = n;
+    for (int I = M - 1; I >= 0; --I) {
+      while (cs > 0 && jcol[cs - 1] >= I * nb) --cs;
+      csI[I] = cs;
+    }
+  }
+  int Itop = M - 1;
+  while (Itop >= 0 && csI[Itop] == n) --Itop;
+  // Lookahead (DESIGN.md s.6 "Complex pencils"): the update of step I is split into the band
+  // (the rows of tile I-1) and the rest; the solve of tile I-1 runs on a high-priority stream
+  // beside the rest.  The scaling decisions use the pending bound (R21), so the solve needs
+  // nothing from the rest; sigma_Y is applied by k_zscale_pending on the update stream.
+  const char* la_env = getenv("ZZ_ZLOOKAHEAD");
+  const bool la = (la_env ? atoi(la_env) != 0 : true) && Itop >= 1;
+  cudaStream_t hp = nullptr;
+  cudaEvent_t ev_band = nullptr, ev_diag = nullptr;
+  struct Guard {
+    cudaStream_t& h; cudaEvent_t& a; cudaEvent_t& b;
+    ~Guard() { if (h) cudaStreamDestroy(h); if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+  } guard{hp, ev_band, ev_diag};
+  if (la) {
+    int lo, hi;
+    ZCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ZCK(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, hi));
+    ZCK(cudaEventCreateWithFlags(&ev_band, cudaEventDisableTiming));
+    ZCK(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
+  }
+  const size_t bsz = 2 * (size_t)nb * n;
+  auto diag = [&](int I, cudaStream_t s) -> cudaError_t {
+    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
     ZDiagParams p;
     p.I = I; p.r0 = r0; p.nt = nt; p.cs = cs; p.n_act = n_act; p.n_sel = n;
     p.S = S; p.lds = lds; p.T = T; p.ldt = ldt; p.X = X; p.ldx = ldx;
@@ -459,24 +505,47 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.e_pend = d_epend; p.nYb = d_nYb;
     p.e_seg = d_eseg + (size_t)I * n;
     p.nrmh_seg = d_nrmh + (size_t)I * n;
-    p.B = d_B;
+    p.B = d_B + (size_t)(I & 1) * bsz;
+    p.sy = d_sy;
     const int grid = std::min((n_act + kZWarps - 1) / kZWarps, nsm);   // one 132 KB CTA per SM
-    k_zdiag<<<grid, kZWarps * 32, smem, st>>>(p);
+    k_zdiag<<<grid, kZWarps * 32, smem, s>>>(p);
     ++launches;
-    ZCK(cudaGetLastError());
-    if (r0 == 0) continue;
-    k_zpanel<<<dim3((r0 + 255) / 256 > 64 ? 64 : (r0 + 255) / 256, 2 * nt), 256, 0, st>>>(S, lds, T, ldt, r0, nt, d_A);
-    ++launches;
-    ZCK(cudaGetLastError());
-    // Y(0:r0, cs:n) <- Y - [S_panel | T_panel] [sigma beta X_I ; -sigma alpha X_I]
-    const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
-    if (cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, r0, n_act, 2 * nt, &mone,
-                    reinterpret_cast<const cuDoubleComplex*>(d_A), r0,
-                    reinterpret_cast<const cuDoubleComplex*>(d_B), 2 * nt, &one,
-                    reinterpret_cast<cuDoubleComplex*>(X + (size_t)cs * ldx), ldx) != CUBLAS_STATUS_SUCCESS)
+    return cudaGetLastError();
+  };
+  const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
+  // Y(row0:row0+rows, cs:n) <- Y - [S_panel | T_panel](row0:row0+rows, :) [sigma beta X_I ; -sigma alpha X_I]
+  auto gemm = [&](int I, int row0, int rows) -> int {
+    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
+    if (cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n_act, 2 * nt, &mone,
+                    reinterpret_cast<const cuDoubleComplex*>(d_A + row0), r0,
+                    reinterpret_cast<const cuDoubleComplex*>(d_B + (size_t)(I & 1) * bsz), 2 * nt, &one,
+                    reinterpret_cast<cuDoubleComplex*>(X + (size_t)cs * ldx + row0), ldx) != CUBLAS_STATUS_SUCCESS)
       return ZZ_ERR_CUDA;
     ++launches;
     info->update_launches++;
+    return 0;
+  };
+  if (Itop >= 0) ZCK(diag(Itop, st));
+  for (int I = Itop; I >= 0; --I) {
+    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
+    if (la && I < Itop) ZCK(cudaStreamWaitEvent(st, ev_diag, 0));
+    if (r0 == 0) break;
+    k_zscale_pending<<<(n_act + 7) / 8, 256, 0, st>>>(X, ldx, r0, cs, n_act, d_sy);
+    k_zpanel<<<dim3((r0 + 255) / 256 > 64 ? 64 : (r0 + 255) / 256, 2 * nt), 256, 0, st>>>(S, lds, T, ldt, r0, nt, d_A);
+    launches += 2;
+    ZCK(cudaGetLastError());
+    if (la) {
+      const int rb = r0 - nb;   // tile I-1 is a full tile
+      if ((r = gemm(I, rb, nb))) return r;
+      ZCK(cudaEventRecord(ev_band, st));
+      ZCK(cudaStreamWaitEvent(hp, ev_band, 0));
+      ZCK(diag(I - 1, hp));
+      ZCK(cudaEventRecord(ev_diag, hp));
+      if (rb > 0 && (r = gemm(I, 0, rb))) return r;
+    } else {
+      if ((r = gemm(I, 0, r0))) return r;
+      ZCK(diag(I - 1, st));
+    }
   }
   k_znorm<<<n, 256, 0, st>>>(X, ldx, nb, n, d_jcol, d_eseg, d_nrmh, col_scale_exp);
   ++launches;

@@ -122,3 +122,24 @@ def test_ztgevc_large_sampled(zz):
     sel[cols] = 1
     ref = oracle.ztgevc(S, T, select=sel)
     assert np.abs(X[:, cols] - ref["X"]).max() < TOL
+
+
+@pytest.mark.parametrize("la", ["0", "1"])
+@pytest.mark.parametrize("stress", [False, True])
+def test_ztgevc_lookahead_modes(zz, monkeypatch, la, stress):
+    """Both schedules (ZZ_ZLOOKAHEAD: the tile solve on a high-priority stream beside the
+    bulk of the previous update, or everything in stream order) against the oracle, on a
+    pencil with selected columns opening mid-wavefront."""
+    monkeypatch.setenv("ZZ_ZLOOKAHEAD", la)
+    m = 700
+    S, T = gen.complex_pencil(m, seed=12, stress=stress)
+    sel = np.ones(m, np.int32)
+    sel[600:] = 0            # the top steps have no active columns
+    sel[::7] = 0
+    X, e = _run(zz, S, T, select=sel, tile=64)
+    ref = oracle.ztgevc(S, T, select=sel)
+    assert np.isfinite(X).all()
+    big = np.abs(ref["X"]) > 1e-200
+    assert np.abs(X[big] - ref["X"][big]).max() < (1e-9 if stress else TOL)
+    if stress:
+        assert (e < 0).any()
