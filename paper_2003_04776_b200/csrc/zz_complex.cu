@@ -29,7 +29,7 @@ namespace zz {
 namespace {
 
 constexpr int kZMaxNB = 64;        // rows per tile: two rows per lane
-constexpr int kZWarps = 16;        // columns (warps) per CTA of k_zdiag
+constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag
 constexpr int kZErrNonfinite = 0;  // status key = 2*row + kind
 constexpr int kZErrCplxDiag = 1;
 
