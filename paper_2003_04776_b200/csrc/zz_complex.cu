@@ -49,6 +49,7 @@ struct ZDiagParams {
   double* nrmh_seg;  // row I
   double2* B;        // 2 nt x n_act, column-major (ld 2 nt)
   int* sy;           // per column: exponent shift of the pending rows (<= 0)
+  double tau_mul;    // 2 (four-multiplication product) or 4 (Gauss 3M, R23)
 };
 
 __device__ __forceinline__ double zabsm(double2 z) { return fmax(fabs(z.x), fabs(z.y)); }
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     const int g = min(ep, e);
     const double yh = ldexp(tipc ? 0.0 : p.nYb[c], g - ep);
     const double xh = ldexp(nx, g - e);
-    const double tau = 2.0 * sums;
+    const double tau = p.tau_mul * sums;
     const int ed = protect_update(yh, tau, xh);
     const int en = g + ed;
     const int sy = en - ep, sx = en - e;
@@ -495,6 +496,10 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     ZCK(cudaEventCreateWithFlags(&ev_band, cudaEventDisableTiming));
     ZCK(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
   }
+  // Gauss's three-multiplication complex product (cublasZgemm3m, default; ZZ_Z3M=0 selects
+  // ZGEMM): 25 % fewer real flops; its (Ar + Ai)(Br + Bi) partial sums are up to twice the
+  // four-multiplication bound, so Algorithm 3's tau doubles (R23)
+  const bool use3m = !(getenv("ZZ_Z3M") && atoi(getenv("ZZ_Z3M")) == 0);
   const size_t bsz = 2 * (size_t)nb * n;
   auto diag = [&](int I, cudaStream_t s) -> cudaError_t {
     const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
@@ -507,6 +512,7 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.nrmh_seg = d_nrmh + (size_t)I * n;
     p.B = d_B + (size_t)(I & 1) * bsz;
     p.sy = d_sy;
+    p.tau_mul = use3m ? 4.0 : 2.0;
     const int grid = std::min((n_act + kZWarps - 1) / kZWarps, nsm);   // one 132 KB CTA per SM
     k_zdiag<<<grid, kZWarps * 32, smem, s>>>(p);
     ++launches;
@@ -516,7 +522,7 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   // Y(row0:row0+rows, cs:n) <- Y - [S_panel | T_panel](row0:row0+rows, :) [sigma beta X_I ; -sigma alpha X_I]
   auto gemm = [&](int I, int row0, int rows) -> int {
     const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
-    if (cublasZgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n_act, 2 * nt, &mone,
+    if ((use3m ? cublasZgemm3m : cublasZgemm)(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n_act, 2 * nt, &mone,
                     reinterpret_cast<const cuDoubleComplex*>(d_A + row0), r0,
                     reinterpret_cast<const cuDoubleComplex*>(d_B + (size_t)(I & 1) * bsz), 2 * nt, &one,
                     reinterpret_cast<cuDoubleComplex*>(X + (size_t)cs * ldx + row0), ldx) != CUBLAS_STATUS_SUCCESS)

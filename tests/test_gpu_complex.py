@@ -124,13 +124,15 @@ def test_ztgevc_large_sampled(zz):
     assert np.abs(X[:, cols] - ref["X"]).max() < TOL
 
 
+@pytest.mark.parametrize("z3m", ["0", "1"])
 @pytest.mark.parametrize("la", ["0", "1"])
 @pytest.mark.parametrize("stress", [False, True])
-def test_ztgevc_lookahead_modes(zz, monkeypatch, la, stress):
+def test_ztgevc_lookahead_modes(zz, monkeypatch, la, stress, z3m):
     """Both schedules (ZZ_ZLOOKAHEAD: the tile solve on a high-priority stream beside the
     bulk of the previous update, or everything in stream order) against the oracle, on a
     pencil with selected columns opening mid-wavefront."""
     monkeypatch.setenv("ZZ_ZLOOKAHEAD", la)
+    monkeypatch.setenv("ZZ_Z3M", z3m)      # ZGEMM or Gauss 3M update (R23)
     m = 700
     S, T = gen.complex_pencil(m, seed=12, stress=stress)
     sel = np.ones(m, np.int32)
