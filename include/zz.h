@@ -193,7 +193,8 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
  *                  normalisation; alpha = beta = 0 gives e_j.                  [args 7,8]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: exponents as zz_tgevc.            [arg 9]
  * Tiles of zz_set_tile() rows when 16..64, else 64.  The update of each step is one complex
- * contraction of K = 2 x tile (cuBLAS ZGEMM over a copy of the S and T panels); the solves,
+ * contraction of K = 2 x tile over a copy of the S and T panels (cuBLAS ZGEMM3M, Gauss's
+ * three-multiplication form, by default; ZGEMM with the environment ZZ_Z3M=0); the solves,
  * scaling decisions, panel copies and normalisation are this library's kernels.  The call
  * allocates its workspace stream-ordered (cudaMallocAsync) and returns after the stream has
  * completed.  Status codes as zz_tgevc (-104 non-finite diagonal entry, -107). */

@@ -8,7 +8,8 @@
 //        and stages the scaled B operand [beta x ; -alpha x];
 //   (3) the update of every pending row above the tile as ONE complex contraction
 //       Y <- Y - [S_panel | T_panel] [sigma beta X_I ; -sigma alpha X_I]   (K = 2 nb),
-//       a cuBLAS ZGEMM on the DMMA pipe over a contiguous copy of the two panels;
+//       a cuBLAS ZGEMM3M (Gauss's three-multiplication form, R23; ZGEMM with ZZ_Z3M=0) on
+//       the DMMA pipe over a contiguous copy of the two panels;
 //   (4) consistency and normalisation (max |Re|+|Im| = 1, ZTGEVC's convention).
 // Readings R18-R21 of DESIGN.md; the pending-row maximum is carried as an upper bound
 // (R21) instead of being measured, so the update needs no epilogue.
