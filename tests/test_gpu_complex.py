@@ -145,3 +145,28 @@ def test_ztgevc_lookahead_modes(zz, monkeypatch, la, stress, z3m):
     assert np.abs(X[big] - ref["X"][big]).max() < (1e-9 if stress else TOL)
     if stress:
         assert (e < 0).any()
+
+
+def test_ztgevc_padded_leading_dimensions(zz):
+    """lds, ldt, ldx larger than m (sub-views of bigger column-major buffers): the same
+    columns as the packed call, and the padding rows of X are not written."""
+    m = 150
+    S, T = gen.complex_pencil(m, seed=13)
+    X0, _ = _run(zz, S, T, tile=32)
+
+    def padded(A, extra):
+        B = torch.zeros((A.shape[1], m + extra), dtype=torch.complex128, device="cuda").t()
+        B[:m] = torch.from_numpy(A).cuda()
+        return B[:m]
+
+    Sd, Td = padded(S, 5), padded(T, 3)
+    Xbuf = torch.full((m, m + 7), 7.0 + 7.0j, dtype=torch.complex128, device="cuda").t()
+    zz.set_tile(32)
+    try:
+        zz.ztgevc(Sd, Td, X=Xbuf[:m])
+        torch.cuda.synchronize()
+    finally:
+        zz.set_tile(0)
+    Xp = Xbuf.cpu().numpy()
+    assert np.array_equal(Xp[:m], X0)
+    assert (Xp[m:] == 7.0 + 7.0j).all()
