@@ -70,4 +70,16 @@ if not args.no_check:
     ref = oracle.ztgevc(S, T, select=sel)
     Xh = X[:, cols].cpu().numpy()
     out["parity_sample"] = {"columns": cols, "max_abs": float(np.abs(Xh - ref["X"]).max()), "tolerance": 1e-10}
+    # the oracle as it stands, on the host cores, on a stratified sample of 96 columns
+    samp = np.unique(np.linspace(0, m - 1, 96).astype(np.int64))
+    sel2 = np.zeros(m, np.int32)
+    sel2[samp] = 1
+    Fs = float(np.sum(8.0 * samp.astype(np.float64) * (samp + 1.0)))
+    t0 = time.time()
+    oracle.ztgevc(S, T, select=sel2)
+    tc = time.time() - t0
+    out["cpu_baseline"] = {"value": Fs / tc * 1e-12, "unit": "TFLOP/s", "cores": os.cpu_count(),
+                           "kind": "oracle", "seconds": tc,
+                           "sample": "%d columns evenly spaced over j of the same pencil, F_sample = %.3g flop"
+                                     % (len(samp), Fs)}
 print(json.dumps(out), flush=True)
