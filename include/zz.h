@@ -192,7 +192,7 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
  *                  max_i (|Re z_i| + |Im z_i|) = 1, from a real positive z_j before
  *                  normalisation; alpha = beta = 0 gives e_j.                  [args 7,8]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: exponents as zz_tgevc.            [arg 9]
- * Tiles of zz_set_tile() rows when 16..64, else 64.  The update of each step is one complex
+ * Tiles of zz_set_tile() rows when it is 32, 48 or 64, else 64 (fastest, profiles/r01o_complex_tile_sweep.txt).  The update of each step is one complex
  * contraction of K = 2 x tile over a copy of the S and T panels (cuBLAS ZGEMM3M, Gauss's
  * three-multiplication form, by default; ZGEMM with the environment ZZ_Z3M=0); the solves,
  * scaling decisions, panel copies and normalisation are this library's kernels.  The call
