@@ -8,9 +8,11 @@ F = sum_c 2 r_c (r_c - 1).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config C4] [--mb 128] [--no-e2e] [--no-cpu]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL): S and T are broadcast from rank 0,
-column blocks are sharded cyclically, X is gathered on rank 0 (all inside the timed
-region); the time is the max over ranks.  `--impl reference` times the oracle (the
+N > 1 runs one rank per GPU (under torchrun, or started by bench.py itself through torchrun
+when --gpus N > 1 is given outside it).  The step is the library's collective zz_tgevc: S and
+T are broadcast from rank 0 by NCCL panel by panel, eigenvalue blocks are owned cyclically,
+X is gathered on rank 0 -- all inside the timed region; the time is the max over ranks
+(torch.distributed/gloo carries only the NCCL id, barriers and the max).  `--impl reference` times the oracle (the
 plain CPU implementation, oracle/) on a bounded sample of the same workload.
 """
 import argparse
@@ -200,6 +202,18 @@ def reference_arm(args):
           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
+def _spawn_ranks(n):
+    """--gpus N > 1 outside torchrun: start N ranks with torchrun (one per GPU), same flags."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -211,16 +225,18 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-blocks", type=int, default=192)
     ap.add_argument("--ref-blocks", type=int, default=24)
-    ap.add_argument("--nb", type=int, default=64, help="column-block width of the multi-GPU shard")
     ap.add_argument("--left", action="store_true", help="also time zz_tgevc_left (left eigenvectors)")
     ap.add_argument("--back", action="store_true",
                     help="also time zz_tgevc_back (back-transformation W = V X, xTGEVC HOWMNY='B')")
     args = ap.parse_args()
-    rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
+    rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
             reference_arm(args)
@@ -230,86 +246,87 @@ def main():
     import paper_2003_04776_b200 as zz
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if local >= torch.cuda.device_count():
+        raise SystemExit("bench.py: rank %d needs GPU %d, only %d visible" % (rank, local, torch.cuda.device_count()))
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # plumbing only (NCCL id, barriers, max over ranks); the data path is the library's NCCL
+        dist.init_process_group("gloo")
+        zz.init_distributed(rank, world, device=local)
+    else:
+        zz.init(local)
     cfg = dict(gen.CONFIGS[args.config])
     m = cfg["m"]
     mb = args.mb
-    zz.init(local)
     zz.set_tile(mb)
-    dev = torch.device("cuda", local)
 
-    # ---- inputs: generated on the host (pinned), resident in HBM before timing ----
-    Sh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True) if rank == 0 else None
-    Th = zz.empty_colmajor(m, m, device="cpu", pin_memory=True) if rank == 0 else None
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v, op="max"):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX if op == "max" else torch.distributed.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- inputs: generated on the host (pinned), resident in rank 0's HBM before timing ----
+    Sh = Th = Sd = Td = None
     if rank == 0:
+        Sh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True)
+        Th = zz.empty_colmajor(m, m, device="cpu", pin_memory=True)
         gen.config(args.config, seed=args.seed, out=(Sh.data_ptr(), Th.data_ptr()))
-    Sd = zz.empty_colmajor(m, m, device=dev)
-    Td = zz.empty_colmajor(m, m, device=dev)
-    if rank == 0:
+        Sd = zz.empty_colmajor(m, m, device=dev)
+        Td = zz.empty_colmajor(m, m, device=dev)
         Sd.copy_(Sh)
         Td.copy_(Th)
         sub = torch.diagonal(Sh, -1).numpy().copy()
     else:
         sub = None
     if world > 1:
-        import torch.distributed as dist
         obj = [sub]
-        dist.broadcast_object_list(obj, src=0)
+        torch.distributed.broadcast_object_list(obj, src=0)
         sub = obj[0]
     blocks = blocks_from_sub(sub, m)
     F = nominal_flops(blocks)
     F_upd, per_launch, M = update_flops(blocks, m, mb)
 
-    Xd = zz.empty_colmajor(m, m, device=dev) if (rank == 0 or world == 1) else None
-    Ed = torch.empty(m, dtype=torch.int32, device=dev)
+    Xd = zz.empty_colmajor(m, m, device=dev) if rank == 0 else None
+    Ed = torch.empty(m, dtype=torch.int32, device=dev) if rank == 0 else None
 
     def step():
-        if world == 1:
+        if rank == 0:
             zz.tgevc(Sd, Td, X=Xd, col_scale_exp=Ed)
         else:
-            from paper_2003_04776_b200 import dist as zdist
+            zz.tgevc_collective(m)
 
-            def compute(S_, T_, sel):
-                return zz.tgevc(S_, T_, select=sel)
-            zdist.tgevc_distributed(Sd, Td, rank, world, compute, nb=args.nb, sub=sub)
-
-    zz.set_timing(True)
+    zz.set_timing(False)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    barrier()
     torch.cuda.synchronize()
     clk = Clocks(local)
     clk.start()
     st = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    upd_ms = 0.0
     launches = 0
     e0.record(st)
     for _ in range(args.steps):
         step()
-        inf = zz.last_info()
-        upd_ms += inf["ms_update"]
-        launches += inf["total_launches"]
+        launches += zz.last_info()["total_launches"]
     e1.record(st)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    barrier()
     clocks = clk.stop()
-    t = e0.elapsed_time(e1) / 1e3 / args.steps
-    if world > 1:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t = float(tt.item())
+    t = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+    launches = int(max_over_ranks(launches, op="sum"))
     value = F / t * 1e-12
-    zz.set_timing(False)
     info = zz.last_info()
-    info_upd_launches = info["update_launches"]
 
     res = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -318,49 +335,75 @@ def main():
                       "seconds_per_step": t, "flops_per_step": F,
                       "fraction_of_fp64_peak": value / (FP64_PEAK * world),
                       "l2": "inputs larger than L2 (S, T %.1f GB each; L2 126 MB)" % (m * m * 8 / 1e9),
-                      "parallelism": "replicated S,T; cyclic column blocks nb=%d" % args.nb if world > 1 else "1 GPU",
+                      "parallelism": ("%d ranks: S,T broadcast from rank 0 by NCCL panel by panel in "
+                                      "consumption order (overlapped), eigenvalue blocks cyclic in groups "
+                                      "of 64 rows, upper parts of X gathered on rank 0 -- all inside the "
+                                      "timed call" % world) if world > 1 else "1 GPU",
                       "phase_ms_last_step": {k: info[k] for k in ("ms_setup", "ms_steps", "ms_normalize")}},
            "gpu_launches": launches}
-    # roofline of the dominant kernel (the robust update, k_update)
-    n_upd_launch = max(1, info_upd_launches)
-    upd_avg = upd_ms / max(1, args.steps * n_upd_launch)
-    if upd_ms > 0:
-        ach = (F_upd / n_upd_launch) / (upd_avg * 1e-3) * 1e-12
-        traffic, tnote = None, None
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_update"]
-            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
-            if tr.get("algorithmic_bytes"):
-                res.setdefault("_traffic_alg", tr["algorithmic_bytes"])
-            tnote = "DRAM bytes of one k_update launch, " + tr["source"]
-        except Exception:
-            pass
-        res["roofline"] = {"bound": "tensor", "kernel": "k_update (DMMA.8x8x4 FP64 contraction)",
-                           "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
-                           "traffic": traffic, "traffic_note": tnote,
-                           "traffic_algorithmic_bytes": res.pop("_traffic_alg", None), "peak_source": PEAK_SRC,
-                           "algorithmic_flops_per_launch": F_upd / n_upd_launch,
-                           "update_launches_per_step": n_upd_launch,
-                           "avg_launch_ms": upd_avg,
-                           "share_of_step": upd_ms / args.steps / (t * 1e3)}
     res["clocks"] = clocks
-    if rank == 0 and world == 1 and not args.no_e2e:
-        # end to end through the public API with HOST buffers (pinned), copies inside
-        Xh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True)
-        Eh = torch.empty(m, dtype=torch.int32).pin_memory()
-        zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
+    if rank == 0 and not args.no_roofline:
+        # roofline of the dominant kernel (the robust update, k_update_t), in a separate pass:
+        # per-launch CUDA events on the launching stream with the lookahead off, so the launches
+        # are serialised and their intervals do not overlap (share_of_step <= 1)
+        zz.set_timing(True)
+        zz.set_lookahead(0)
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        if world == 1:
+            r0.record(st)
+            zz.tgevc(Sd, Td, X=Xd, col_scale_exp=Ed)
+            r1.record(st)
+            torch.cuda.synchronize()
+            inf = zz.last_info()
+            t_r = r0.elapsed_time(r1)
+            n_upd = max(1, inf["update_launches"])
+            upd_avg = inf["ms_update"] / n_upd
+            ach = (F_upd / n_upd) / (upd_avg * 1e-3) * 1e-12
+            traffic, tnote, talg = None, None, None
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_update"]
+                traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+                talg = tr.get("algorithmic_bytes")
+                tnote = "DRAM bytes of one k_update_t launch, " + tr["source"]
+            except Exception:
+                pass
+            res["roofline"] = {"bound": "tensor", "kernel": "k_update_t (DMMA.8x8x4 FP64 contraction)",
+                               "achieved": ach, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": ach / FP64_PEAK,
+                               "traffic": traffic, "traffic_note": tnote, "traffic_algorithmic_bytes": talg,
+                               "peak_source": PEAK_SRC,
+                               "algorithmic_flops_per_launch": F_upd / n_upd,
+                               "update_launches_per_step": n_upd, "avg_launch_ms": upd_avg,
+                               "timing": "separate pass after the timed region, lookahead off (serialised "
+                                         "launches), CUDA events on the launching stream",
+                               "pass_ms": t_r, "share_of_step": inf["ms_update"] / t_r}
+        zz.set_timing(False)
+        zz.set_lookahead(1)
+    if not args.no_e2e:
+        # end to end through the public API with HOST buffers (pinned), copies inside the timed
+        # region (collective zz_tgevc_host for N > 1: rank 0's panels go up and out by broadcast)
+        Xh = zz.empty_colmajor(m, m, device="cpu", pin_memory=True) if rank == 0 else None
+        Eh = torch.empty(m, dtype=torch.int32).pin_memory() if rank == 0 else None
+
+        def step_host():
+            if rank == 0:
+                zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
+            else:
+                zz.tgevc_host_collective(m)
+        step_host()
         ks = max(1, args.e2e_steps)
+        barrier()
         t0 = time.perf_counter()
         for _ in range(ks):
-            zz.tgevc_host(Sh, Th, X=Xh, col_scale_exp=Eh)
-        te = (time.perf_counter() - t0) / ks
+            step_host()
+        te = max_over_ranks((time.perf_counter() - t0) / ks)
         res["e2e"] = {"value": F / te * 1e-12, "unit": "TFLOP/s", "seconds_per_step": te,
                       "h2d_bytes_per_step": int(2 * STAGED_BYTES), "d2h_bytes_per_step": int(D2H_BYTES),
                       "steps": ks, "api": "zz_tgevc_host (pinned host S, T, X; S and T staged by tile "
                                           "column in consumption order, upper part only, overlapped; "
                                           "X downloaded upper part only, zeros written by host threads "
-                                          "during the solve)"}
-        Xd_check = Xd
+                                          "during the solve)" + ("; collective over %d ranks" % world if world > 1 else "")}
+        Xh = Eh = None
     if rank == 0 and world == 1 and not args.no_cpu:
         Sn, Tn = Sh.numpy(), Th.numpy()
         f, dt, cores, sel, r = run_oracle_sample(Sn, Tn, blocks, m, args.cpu_blocks)
@@ -409,8 +452,8 @@ def main():
     if rank == 0 and world == 1 and args.back:
         # back-transformation leg (a separate capability, not part of the headline metric):
         # V is a seeded Gaussian N(0, 1/m) made on the device -- the work does not depend on
-        # V being orthogonal; the product is the DGEMM column blocks of zz_tgevc_back
-        Xd = Xd_check = None
+        # V being orthogonal
+        Xd = None
         torch.cuda.empty_cache()
         gv = torch.Generator(device=dev)
         gv.manual_seed(args.seed + 7)
@@ -433,15 +476,15 @@ def main():
         tb = b0.elapsed_time(b1) / 1e3 / kb
         ms_back /= kb
         res["backtransform"] = {
-            "api": "zz_tgevc_back (solve + W = V X in 256-column DGEMM blocks with K = 1 + max r_c + LAPACK normalisation)",
+            "api": "zz_tgevc_back (solve + W = V X over the triangular K range + LAPACK normalisation)",
             "seconds_per_step": tb, "ms_back": ms_back, "flops_back": F_back,
             "tflops_back": F_back / (ms_back * 1e-3) * 1e-12,
-            "frac_of_dgemm_peak": F_back / (ms_back * 1e-3) * 1e-12 / 35.5,
-            "dgemm_peak_source": "cuBLAS DGEMM 8192^3 measured 35.5 TFLOP/s (profiles/r01_fp64_peak.json)",
+            "frac_of_fp64_peak": F_back / (ms_back * 1e-3) * 1e-12 / FP64_PEAK,
             "V": "seeded Gaussian N(0, 1/m) on the device (timing only)"}
     if rank == 0:
         emit(res)
     if world > 1:
+        barrier()
         torch.distributed.destroy_process_group()
 
 

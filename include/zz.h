@@ -29,10 +29,16 @@
  *  -107   zz_ztgevc: a diagonal entry of T is not real
  * There is no CPU fallback: without a CUDA device every call returns -100 or -103.
  *
- * Threading.  One context per host thread (thread-local), bound to one device.  Calls on
- * a context are not reentrant.  Multi-GPU use (one process per GPU) shards eigenvector
- * column blocks through `select` (see paper_2003_04776_b200/dist.py); no call of this
- * library communicates between devices.
+ * Threading and multi-GPU.  One context per host thread (thread-local), bound to one device.
+ * Calls on a context are not reentrant.  Multi-GPU (one process per GPU):
+ * zz_get_unique_id on rank 0, the 128 bytes shipped to the other ranks by the caller (e.g.
+ * torch.distributed), zz_init(device, nranks, rank, id) on every rank; zz_tgevc and
+ * zz_tgevc_host are then collective.  The task graph of the method is the disjoint union of
+ * per-column-block subgraphs: eigenvalue blocks are owned in groups of 64 rows
+ * cyclically over the ranks, every rank runs the whole bottom-up wavefront over its own
+ * columns, S and T are broadcast from rank 0 (NCCL, panel by panel in the order the wavefront
+ * consumes them, upper part only, overlapped with the solve), and the finished columns (rows
+ * 0 .. r_c) are gathered on rank 0.  X is bitwise independent of the number of ranks.
  */
 #ifndef ZZ_H
 #define ZZ_H
@@ -43,12 +49,14 @@ extern "C" {
 
 #define ZZ_OK 0
 #define ZZ_ERR_CUDA (-100)
+#define ZZ_ERR_NCCL (-101)
 #define ZZ_ERR_NOMEM (-102)
 #define ZZ_ERR_NOCTX (-103)
 #define ZZ_ERR_NONFINITE (-104)
 #define ZZ_ERR_OVERLAP (-105)
 #define ZZ_ERR_TILE (-106)
 #define ZZ_ERR_CPLXDIAG (-107)
+#define ZZ_ERR_SHARD (-108)
 
 /* Statistics of the last zz_tgevc call of this thread's context. */
 typedef struct zz_info {
@@ -69,11 +77,45 @@ typedef struct zz_info {
   double ms_normalize;     /* consistency and normalisation */
   double ms_update;        /* summed device time of the robust-update kernels (if timed) */
   double ms_back;          /* zz_tgevc_back: back-transformation GEMMs + normalisation */
+  /* DEVICE views into the library workspace, n_sel doubles each in output
+   * column order; valid until the next call on this context; NULL when n_sel == 0 and after
+   * zz_tgevc_left / zz_ztgevc.  Read-only for the caller.
+   *   logmax   L_c = log2(max_i measure of the stored column before normalisation) - e_c,
+   *            i.e. log2 of the max measure of the tip-normalised eigenvector (x_r = 1,
+   *            PAPER.md:152; Definition 1); measure |x_i| (real) or
+   *            |x_i| + |y_i| (pair); -inf for an all-zero column (never produced)
+   *   a, b, beta  the power-of-two normalised eigenvalue pair (alpha = a + i b, PAPER.md:72,
+   *            79-99) the pivots beta S_ii - alpha T_ii were formed with; both columns of a
+   *            pair carry the same values (b > 0); real columns have b = 0 */
+  const double* d_logmax;
+  const double* d_a;
+  const double* d_b;
+  const double* d_beta;
 } zz_info_t;
 
-/* Create (or re-bind) this thread's context on CUDA device `device`.
- * Returns 0 or -100 (no such device / CUDA error). */
-int zz_init(int device);
+/* 128-byte NCCL unique id for zz_init (call on rank 0, ship the bytes to every rank).
+ * Returns 0, -1 (id NULL) or -101 (NCCL not available: it is loaded at run time). */
+int zz_get_unique_id(unsigned char* id);
+
+/* Create (or re-bind) this thread's context on CUDA device `device` as rank `rank` of
+ * `nranks` processes (one per GPU).  id: the 128 bytes of zz_get_unique_id, or NULL iff
+ * nranks == 1 (no communicator).  With an id the call is collective (ncclCommInitRank):
+ * every rank blocks until all have joined.  nranks = 1 with an id creates a one-rank
+ * communicator: zz_tgevc then runs its collective code path on one GPU (broadcast and
+ * gather to itself; used by the tests).  Returns 0, -2 (nranks < 1), -3 (bad rank),
+ * -4 (id NULL with nranks > 1), -100 (no such device) or -101 (NCCL). */
+int zz_init(int device, int nranks, int rank, const unsigned char* id);
+
+/* One-GPU emulation of a rank's share (single-rank contexts only): subsequent zz_tgevc calls
+ * compute only the columns that rank p of P would own (eigenvalue blocks with first row j
+ * such that (j / 64) mod P == p) and write them into their global positions of X (the
+ * columns of X that belong to other shards are not written; col_scale_exp likewise).
+ * Running p = 0 .. P-1 into one X assembles, bit for bit, the X of a plain call.  With a
+ * one-rank communicator, p != 0 also takes the non-root data path (S, T from the broadcast
+ * copy, columns through NCCL send/recv).  zz_set_shard(0, 1) restores the plain call.
+ * zz_tgevc_host rejects an emulated shard (-108).  Returns 0, -1 / -2 (bad p / P), -103,
+ * or -108 (the context has nranks > 1). */
+int zz_set_shard(int p, int P);
 
 /* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = legacy default
  * stream).  The stream is borrowed, never destroyed.  Returns 0 or -103. */
@@ -126,6 +168,12 @@ int zz_set_lookahead(int mode);
  * Work runs on the context's stream; the call returns after the stream has completed.
  * Ownership: S, T, X, col_scale_exp are caller-owned; the library owns a workspace grown
  * on demand and freed by zz_finalize.
+ * Multi-rank context (zz_init with nranks > 1): collective; every rank passes the same m and
+ * select; rank 0 passes S, T, X, col_scale_exp, the other ranks' pointer and leading-
+ * dimension arguments are ignored (pass NULL / 0).  On return rank 0 holds the full X.  The
+ * non-root ranks keep a library copy of S and T (2 m^2 doubles) and of their own columns.
+ * Status -101 for an NCCL failure.  zz_last_info describes the rank's own columns (n_sel =
+ * local columns, device views NULL).
  */
 int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,
              double* X, int ldx, int* col_scale_exp);
@@ -133,7 +181,10 @@ int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const in
 /* zz_tgevc_host: the same operation with HOST S, T, X, col_scale_exp (pinned memory
  * recommended).  The library stages S and T into device memory, solves, and copies X and
  * col_scale_exp back, all on the context's stream (end-to-end path of bench.py).
- * Arguments and status codes as zz_tgevc. */
+ * Arguments and status codes as zz_tgevc; collective on a multi-rank context (rank 0's host
+ * panels go up and out by broadcast as they arrive).  On a nonzero status the rows of X
+ * below each selected column's diagonal block may already have been set to zero (they are
+ * written by host threads while the device solves); nothing else of X is written. */
 int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select,
                   double* X, int ldx, int* col_scale_exp);
 
@@ -210,6 +261,13 @@ int zz_count_columns(int m, const double* S_host, int lds, const int* select);
  * entries, tile_start[M] = m) and returns M, or -105 / -106.  tile_start must hold
  * m/(mb-1)+2 ints. */
 int zz_partition(int m, const double* sub, int mb, int* tile_start);
+
+/* Host-only ownership rule of the multi-GPU path: given the m-1
+ * subdiagonal entries sub[j] = S(j+1,j) (HOST), the HOST select (or NULL) and P shards,
+ * writes the global output column indices owned by shard p (ascending; eigenvalue blocks with
+ * first row j such that (j / 64) mod P == p; a pair's two columns stay together) to cols (may
+ * be NULL) and returns their number, or -105 / a negative argument index. */
+int zz_shard_columns(int m, const double* sub, const int* select, int P, int p, int* cols);
 
 /* Statistics of the last call.  Returns 0 or -103. */
 int zz_last_info(zz_info_t* out);

@@ -26,9 +26,11 @@ STATUS = {
     -105: "overlapping 2x2 blocks",
     -106: "unsupported tile size",
     -107: "a diagonal entry of T is not real (zz_ztgevc)",
+    -101: "NCCL error",
+    -108: "shard emulation not allowed here",
 }
 
-EXPORTS = ["zz_init", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left", "zz_ztgevc",
+EXPORTS = ["zz_get_unique_id", "zz_init", "zz_set_shard", "zz_shard_columns", "zz_set_stream", "zz_set_tile", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left", "zz_ztgevc",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -48,10 +50,46 @@ class Info(ctypes.Structure):
                 ("fused_pairs", ctypes.c_int), ("lookahead_redo", ctypes.c_int),
                 ("ms_setup", ctypes.c_double), ("ms_steps", ctypes.c_double),
                 ("ms_normalize", ctypes.c_double), ("ms_update", ctypes.c_double),
-                ("ms_back", ctypes.c_double)]
+                ("ms_back", ctypes.c_double),
+                ("d_logmax", ctypes.c_void_p), ("d_a", ctypes.c_void_p), ("d_b", ctypes.c_void_p),
+                ("d_beta", ctypes.c_void_p)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_cudart_lib = None
+
+
+def _d2h(ptr, nbytes):
+    """copy `nbytes` of device memory at `ptr` to a new host bytes buffer (cudaMemcpy)"""
+    global _cudart_lib
+    if _cudart_lib is None:
+        import glob
+        cands = []
+        try:
+            import nvidia.cuda_runtime as cr
+            for d in cr.__path__:
+                cands += sorted(glob.glob(os.path.join(d, "lib", "libcudart.so*")))
+        except Exception:
+            pass
+        cands += ["libcudart.so.12", "libcudart.so"]
+        for c in cands:
+            try:
+                _cudart_lib = ctypes.CDLL(c)
+                break
+            except OSError:
+                continue
+        if _cudart_lib is None:
+            raise ImportError("libcudart not found")
+        _cudart_lib.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        _cudart_lib.cudaMemcpy.restype = ctypes.c_int
+    buf = ctypes.create_string_buffer(max(int(nbytes), 1))
+    if nbytes:
+        st = _cudart_lib.cudaMemcpy(buf, ctypes.c_void_p(ptr), int(nbytes), 2)
+        if st != 0:
+            raise RuntimeError("cudaMemcpy (device views) failed: %d" % st)
+    return buf.raw[:nbytes]
 
 
 def library_path():
@@ -75,7 +113,10 @@ def load(build_if_missing=True):
     lib = ctypes.CDLL(_SO)
     vp, ci = ctypes.c_void_p, ctypes.c_int
     sig = {
-        "zz_init": ([ci], ci),
+        "zz_get_unique_id": ([vp], ci),
+        "zz_init": ([ci, ci, ci, vp], ci),
+        "zz_set_shard": ([ci, ci], ci),
+        "zz_shard_columns": ([ci, vp, vp, ci, ci, vp], ci),
         "zz_set_stream": ([vp], ci),
         "zz_set_tile": ([ci], ci),
         "zz_set_timing": ([ci], ci),
@@ -108,15 +149,57 @@ def _check(st, what):
 _inited = {}
 
 
-def init(device=None):
-    """Create this thread's context on `device` (default: torch's current device)."""
+def init(device=None, nranks=1, rank=0, unique_id=None):
+    """Create this thread's context on `device` (default: torch's current device) as rank
+    `rank` of `nranks` (include/zz.h zz_init).  unique_id: the 128 bytes of get_unique_id()
+    on rank 0 (required for nranks > 1; with nranks == 1 it creates a one-rank communicator)."""
     import torch
     if device is None:
         device = torch.cuda.current_device()
     lib = load()
-    _check(lib.zz_init(int(device)), "zz_init")
+    uid = None
+    if unique_id is not None:
+        if len(unique_id) != 128:
+            raise ValueError("unique_id must be 128 bytes")
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(lib.zz_init(int(device), int(nranks), int(rank), uid), "zz_init")
     _inited[device] = True
     return device
+
+
+def get_unique_id():
+    """128-byte NCCL unique id (rank 0; ship it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().zz_get_unique_id(buf), "zz_get_unique_id")
+    return buf.raw
+
+
+def init_distributed(rank, world, device=None, group=None):
+    """Multi-GPU context: rank 0 creates the NCCL id, torch.distributed ships it (plumbing
+    only), every rank calls zz_init(device, world, rank, id).  Collective."""
+    import torch.distributed as dist
+    obj = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return init(device, world, rank, obj[0])
+
+
+def set_shard(p, P):
+    """One-GPU emulation of rank p's share of P (include/zz.h zz_set_shard); (0, 1) resets."""
+    _check(load().zz_set_shard(int(p), int(P)), "zz_set_shard")
+
+
+def shard_columns(sub, m, P, p, select=None):
+    """Global output columns owned by shard p of P (host-only ownership rule of the library,
+    include/zz.h zz_shard_columns)."""
+    import numpy as np
+    s = np.ascontiguousarray(np.asarray(sub, dtype=np.float64).reshape(-1))
+    sel = _sel_array(select, m)
+    out = np.zeros(max(m, 1), np.int32)
+    n = load().zz_shard_columns(m, s.ctypes.data if s.size else None, None if sel is None else sel.ctypes.data,
+                                int(P), int(p), out.ctypes.data)
+    if n < 0:
+        raise ZZError(n, "zz_shard_columns")
+    return out[:n].copy()
 
 
 def set_tile(mb):
@@ -141,6 +224,20 @@ def last_info():
     inf = Info()
     _check(load().zz_last_info(ctypes.byref(inf)), "zz_last_info")
     return inf.as_dict()
+
+
+def last_views():
+    """Host copies of the device views of the last call (include/zz.h zz_info_t): a dict of
+    numpy arrays logmax (L_c), a, b, beta, n_sel entries each, or None where the view is NULL."""
+    import numpy as np
+    inf = Info()
+    _check(load().zz_last_info(ctypes.byref(inf)), "zz_last_info")
+    n = inf.n_sel
+    out = {}
+    for k in ("logmax", "a", "b", "beta"):
+        ptr = getattr(inf, "d_" + k)
+        out[k] = None if not ptr else np.frombuffer(_d2h(ptr, 8 * n), dtype=np.float64).copy()
+    return out
 
 
 def _ld_colmajor(A, m, what):
@@ -240,6 +337,35 @@ def tgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None, n_sel=None
                      col_scale_exp.data_ptr() if n_sel > 0 else None)
     _check(r, "zz_tgevc")
     return X, col_scale_exp
+
+
+def tgevc_collective(m, S=None, T=None, select=None, X=None, col_scale_exp=None, stream=None):
+    """zz_tgevc on a multi-rank context (init_distributed): rank 0 passes S, T (CUDA float64
+    column-major) and gets (X, col_scale_exp); the other ranks pass only m (and the same
+    select) and get (None, None)."""
+    import torch
+    lib = load()
+    if S is not None:
+        return tgevc(S, T, select=select, X=X, col_scale_exp=col_scale_exp, stream=stream)
+    sel = _sel_array(select, m)
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib.zz_set_stream(ctypes.c_void_p(st.cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc(int(m), None, 0, None, 0, None if sel is None else sel.ctypes.data, None, 0, None)
+    _check(r, "zz_tgevc")
+    return None, None
+
+
+def tgevc_host_collective(m, S=None, T=None, select=None, X=None, col_scale_exp=None):
+    """zz_tgevc_host on a multi-rank context: rank 0 passes host S, T (and X); others only m."""
+    import torch
+    lib = load()
+    if S is not None:
+        return tgevc_host(S, T, select=select, X=X, col_scale_exp=col_scale_exp)
+    sel = _sel_array(select, m)
+    _check(lib.zz_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "zz_set_stream")
+    r = lib.zz_tgevc_host(int(m), None, 0, None, 0, None if sel is None else sel.ctypes.data, None, 0, None)
+    _check(r, "zz_tgevc_host")
+    return None, None
 
 
 def ztgevc(S, T, select=None, X=None, col_scale_exp=None, stream=None):

@@ -8,7 +8,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libzz.so")
-SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu", "zz_back.cu", "zz_left.cu", "zz_complex.cu"]
+SRCS = ["zz_api.cu", "zz_kernels.cu", "zz_update.cu", "zz_diag3.cu", "zz_back.cu", "zz_left.cu", "zz_complex.cu", "zz_comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -46,7 +46,7 @@ def build(force=False, verbose=False):
     objs = [obj for _, obj, _ in results]
     cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
     r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO + ".tmp"] + objs
-                       + ["-L" + cudalib, "-lcublas", "-Xlinker", "-rpath", "-Xlinker", cudalib],
+                       + ["-L" + cudalib, "-lcublas", "-ldl", "-Xlinker", "-rpath", "-Xlinker", cudalib],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)

@@ -75,6 +75,11 @@ struct Context {
   Buf sYb, nYb;            // second sY set; per-column bound of the pending rows (lookahead)
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
+  // communicator (zz_init with an id) and the shard of this rank
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int shard_p = 0, shard_P = 1;   // zz_set_shard: one-GPU emulation of a rank's share
+  Buf Sw, Tw, Xloc, Eloc, bbuf, sendb, recvb, gtab, subd;
   Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
   cublasHandle_t blas = nullptr;          // the back-transformation GEMMs
   std::vector<int> last_col_r;            // r_c of the last call's columns (host)
@@ -99,6 +104,12 @@ struct Context {
     if (hi) cudaStreamDestroy(hi);
     hi = nullptr;
     Xb.release();
+    Buf* cb[] = {&Sw, &Tw, &Xloc, &Eloc, &bbuf, &sendb, &recvb, &gtab, &subd};
+    for (Buf* b : cb) b->release();
+    if (comm) {
+      if (const NcclApi* api = nccl_api()) api->commDestroy(comm);
+      comm = nullptr;
+    }
     Sl.release();
     Tl.release();
     El.release();
@@ -191,22 +202,39 @@ int make_map(Context* c, CUtensorMap* tm, const double* A, long long lda, int m)
   return r == CUDA_SUCCESS ? 0 : ZZ_ERR_CUDA;
 }
 
-// zz_tgevc_host: S and T arrive from host memory panel by panel, in the order the wavefront
-// consumes them (tile columns M-1 .. 0, upper part and subdiagonal only), on a copy stream;
-// step I waits for panel I only, so the copies overlap the solve.
-struct HostStage {
-  const double* Sh;
-  long long ldsh;
-  const double* Th;
-  long long ldth;
-  cudaStream_t copy;
-  std::vector<cudaEvent_t>* ev;
+// Staged panels: S and T arrive tile column by tile column in the order the wavefront
+// consumes them (tile columns M-1 .. 0, upper part and subdiagonal only) on a separate
+// stream -- from host memory (zz_tgevc_host) and/or by an NCCL broadcast from rank 0 (the
+// collective zz_tgevc); step I waits for panel I only, so the transfers
+// overlap the solve.  The pairs and panel norms of panel I are computed when it lands and
+// the status checks are deferred to the end of the wavefront.
+struct Feed {
+  const double* Sh = nullptr;  // host source of S, T (zz_tgevc_host), or null
+  long long ldsh = 0;
+  const double* Th = nullptr;
+  long long ldth = 0;
+  const double* sub = nullptr; // host copy of the subdiagonal (m-1 entries), if known
+  cudaStream_t copy = nullptr; // stream of the transfers
+  std::vector<cudaEvent_t>* ev = nullptr;
+  ncclComm_t comm = nullptr;   // NCCL broadcast of the panels from rank 0
+  const NcclApi* api = nullptr;
+  bool root = true;            // this rank sends (its S, T are complete: Ssrc, Tsrc)
+  const double* Ssrc = nullptr;  // root: the device S, T the panels are packed from
+  long long ldss = 0;
+  const double* Tsrc = nullptr;
+  long long ldts = 0;
+  double* bbuf = nullptr;      // contiguous staging of one panel pair (comm only)
+  bool wait = true;            // the steps wait for the panel events
 };
 
 // The solve on device pointers.  S/T are const; X, cse written.
 int tgevc_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
-                 const int* select, double* X, long long ldx, int* cse, const HostStage* hs = nullptr) {
+                 const int* select, double* X, long long ldx, int* cse, const Feed* hs = nullptr) {
   cudaStream_t st = c->stream;
+  // the caller's X: the recomputations below (pre-scale of the host path, lookahead redo)
+  // start again from it, not from the aligned internal buffer X may be swapped for
+  double* const X_call = X;
+  const long long ldx_call = ldx;
   zz_info_t info;
   memset(&info, 0, sizeof(info));
   info.m = m;
@@ -219,7 +247,9 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   int launches = 0;
   // ---- a1: structure scan (one host sync; none when S is on the host) ----
   std::vector<double> sub((size_t)std::max(m - 1, 1), 0.0);
-  if (hs) {
+  if (hs && hs->sub) {
+    for (int j = 0; j + 1 < m; ++j) sub[j] = hs->sub[j];
+  } else if (hs && hs->Sh) {
     for (int j = 0; j + 1 < m; ++j) sub[j] = hs->Sh[(size_t)j * hs->ldsh + j + 1];
   } else {
     CK(c->sub.ensure(sizeof(double) * (size_t)std::max(m, 1)));
@@ -292,7 +322,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   const int n = std::max(n_sel, 1);
   const int nks_max = ceil_div(mb, kBK);
   const int n_ntiles_all = ceil_div(n, kBN);
-  CK(c->colf.ensure(sizeof(double) * 3 * (size_t)n));
+  CK(c->colf.ensure(sizeof(double) * 4 * (size_t)n));
   CK(c->coli.ensure(sizeof(int) * 9 * (size_t)n));
   CK(c->items.ensure(sizeof(int) * 2 * (size_t)std::max(n_items, 1)));
   CK(c->tiles.ensure(sizeof(int) * (size_t)(M + 1)));
@@ -309,6 +339,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.col_a = c->colf.as<double>();
   P.col_b = P.col_a + n;
   P.col_beta = P.col_b + n;
+  P.logmax = P.col_beta + n;
   P.col_kind = c->coli.as<int>();
   P.col_r = P.col_kind + n;
   P.col_tile = P.col_r + n;
@@ -374,10 +405,35 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     }
     for (int I = M - 1; I >= 0; --I) {
       const int rows = std::min(ts[I + 1] + 1, m), ncol = ts[I + 1] - ts[I];
-      CK(cudaMemcpy2DAsync((void*)(S + (size_t)ts[I] * lds), (size_t)lds * 8, hs->Sh + (size_t)ts[I] * hs->ldsh,
-                           (size_t)hs->ldsh * 8, (size_t)rows * 8, ncol, cudaMemcpyHostToDevice, hs->copy));
-      CK(cudaMemcpy2DAsync((void*)(T + (size_t)ts[I] * ldt), (size_t)ldt * 8, hs->Th + (size_t)ts[I] * hs->ldth,
-                           (size_t)hs->ldth * 8, (size_t)rows * 8, ncol, cudaMemcpyHostToDevice, hs->copy));
+      double* Sp = (double*)(S + (size_t)ts[I] * lds);
+      double* Tp = (double*)(T + (size_t)ts[I] * ldt);
+      if (hs->Sh) {
+        // host panel -> rank 0's device copy (Ssrc, Tsrc)
+        CK(cudaMemcpy2DAsync((void*)(hs->Ssrc + (size_t)ts[I] * hs->ldss), (size_t)hs->ldss * 8,
+                             hs->Sh + (size_t)ts[I] * hs->ldsh, (size_t)hs->ldsh * 8, (size_t)rows * 8, ncol,
+                             cudaMemcpyHostToDevice, hs->copy));
+        CK(cudaMemcpy2DAsync((void*)(hs->Tsrc + (size_t)ts[I] * hs->ldts), (size_t)hs->ldts * 8,
+                             hs->Th + (size_t)ts[I] * hs->ldth, (size_t)hs->ldth * 8, (size_t)rows * 8, ncol,
+                             cudaMemcpyHostToDevice, hs->copy));
+      }
+      if (hs->comm) {
+        // one contiguous buffer [S panel | T panel] per broadcast (rows x ncol each)
+        const size_t half = (size_t)rows * ncol;
+        if (hs->root) {
+          CK(cudaMemcpy2DAsync(hs->bbuf, (size_t)rows * 8, hs->Ssrc + (size_t)ts[I] * hs->ldss,
+                               (size_t)hs->ldss * 8, (size_t)rows * 8, ncol, cudaMemcpyDeviceToDevice, hs->copy));
+          CK(cudaMemcpy2DAsync(hs->bbuf + half, (size_t)rows * 8, hs->Tsrc + (size_t)ts[I] * hs->ldts,
+                               (size_t)hs->ldts * 8, (size_t)rows * 8, ncol, cudaMemcpyDeviceToDevice, hs->copy));
+        }
+        if (hs->api->broadcast(hs->bbuf, hs->bbuf, 2 * half, ncclFloat64, 0, hs->comm, hs->copy) != ncclSuccess)
+          return ZZ_ERR_NCCL;
+        if (!hs->root || Sp != hs->Ssrc + (size_t)ts[I] * hs->ldss) {
+          CK(cudaMemcpy2DAsync(Sp, (size_t)lds * 8, hs->bbuf, (size_t)rows * 8, (size_t)rows * 8, ncol,
+                               cudaMemcpyDeviceToDevice, hs->copy));
+          CK(cudaMemcpy2DAsync(Tp, (size_t)ldt * 8, hs->bbuf + half, (size_t)rows * 8, (size_t)rows * 8, ncol,
+                               cudaMemcpyDeviceToDevice, hs->copy));
+        }
+      }
       CK(cudaEventRecord((*hs->ev)[I], hs->copy));
     }
   }
@@ -543,7 +599,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   auto panel_ready = [&](int I) -> int {
     if (!hs) return 0;
     // panel I has arrived: its eigenvalue pairs and column-panel norms
-    CK(cudaStreamWaitEvent(ms, (*hs->ev)[I], 0));
+    if (hs->wait) CK(cudaStreamWaitEvent(ms, (*hs->ev)[I], 0));
     CK(launch_pairs(Su, ldsu, Tu, ldtu, tile_blk[I], tile_blk[I + 1] - tile_blk[I], P, ms));
     CK(launch_panel_norms(Su, ldsu, Tu, ldtu, M, ts.data(), P, ms, I, 1));
     launches += 2;
@@ -731,7 +787,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
         const int rb = ts[L - len_next];        // rows [rb, ts[L]): the next group's band
         UpdParams fb = fu;                    // the band first, on the chain's stream
         fb.row_lo = rb;
-        fb.max_row = 0;
+        // the band part measures rows [rb, ts[L-1]) and the bulk rows [0, rb) into the same
+        // buffer (atomicMax: order-independent), so the next group's last decision reads the
+        // maximum over [0, ts[L-1]) exactly as in the plain schedule (base_up(L).max_row)
+        fb.max_row = ts[L - 1];
         if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
         cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
         CK(cudaEventRecord(ev_dec, ms));
@@ -785,6 +844,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   if (Xout)
     CK(cudaMemcpy2DAsync(Xout, sizeof(double) * ldxo, X, sizeof(double) * ldx, sizeof(double) * m, n_sel,
                          cudaMemcpyDeviceToDevice, st));
+  // every staged transfer (the last one is panel 0) completes before the call returns
+  if (hs && M > 0) CK(cudaStreamWaitEvent(st, (*hs->ev)[0], 0));
   CK(cudaEventRecord(c->e3, st));
   int stat[16];
   CK(cudaMemcpyAsync(stat, P.status, sizeof(stat), cudaMemcpyDeviceToHost, st));
@@ -805,20 +866,26 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       mdS = std::max(mdS, nrm[2 * M + I]); mdT = std::max(mdT, nrm[3 * M + I]);
     }
     if (bS + mdS > 0x1p1020 || bT + mdT > 0x1p1020)
-      return tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, cse, nullptr);
+      return tgevc_device(c, m, S, lds, T, ldt, select, X_call, ldx_call, cse, nullptr);
   }
   if (la && stat[6]) {
     // a group's first decision on the recorded bound would have scaled where the measured
     // maximum may not: recompute without lookahead (bitwise the plain schedule's result)
     const int saved = c->lookahead;
     c->lookahead = 0;
-    const int rr = tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, cse, nullptr);
+    const int rr = tgevc_device(c, m, S, lds, T, ldt, select, X_call, ldx_call, cse, nullptr);
     c->lookahead = saved;
     c->info.lookahead_redo = 1;
     return rr;
   }
   info.n_scaled = stat[4];
   info.min_exp = stat[5];
+  if (n_sel > 0) {
+    info.d_logmax = P.logmax;
+    info.d_a = P.col_a;
+    info.d_b = P.col_b;
+    info.d_beta = P.col_beta;
+  }
   info.update_launches = n_upd;
   info.fused_pairs = n_fused;
   info.total_launches = launches;
@@ -906,6 +973,201 @@ int tgevc_left_device(Context* c, int m, const double* S, long long lds, const d
   CK(launch_left_gather(c->Xb.as<double>(), ldf, Y, ldy, m, n_sel, c->coli.as<int>(), c->El.as<int>(), cse, st));
   CK(cudaStreamSynchronize(st));
   c->info.total_launches += 3;
+  // the device views describe the flipped pencil's columns: not exported for left vectors
+  c->info.d_logmax = c->info.d_a = c->info.d_b = c->info.d_beta = nullptr;
+  return 0;
+}
+
+// ---- the sharded / collective solve ----
+// The eigenvalue blocks are owned in groups of kShardNB rows, cyclically over P shards (block
+// with first row j -> shard (j / kShardNB) mod P: triangular load balance).  Every shard runs
+// the full bottom-up wavefront over its own columns only -- the task graph is the disjoint
+// union of per-column-block subgraphs, and a column's arithmetic does not depend
+// on which other columns are computed, so X is bitwise independent of P.  With a communicator,
+// S and T come from rank 0 by NCCL broadcast panel by panel in consumption order (I = M-1 .. 0,
+// upper part and subdiagonal only; step I waits for panel I), and the finished columns -- their
+// upper parts only, rows 0 .. r_c -- are gathered on rank 0 and written into the caller's X
+// (zeros below).  Without one (zz_set_shard on a single GPU) the shard's columns are written
+// into their global positions of X and the others are left untouched.
+struct ShardCol { int g, r; };
+
+// Owner of every selected eigenvalue block (first row j -> shard (j / kShardNB) mod P): the
+// global output columns (block order) and last rows of each shard, and shard p's select mask.
+void shard_owners(int m, const std::vector<int>& bs, const std::vector<int>& bz, const int* select, int P, int p,
+                  std::vector<std::vector<ShardCol>>& cols, std::vector<int>& sel_loc) {
+  cols.assign((size_t)P, {});
+  sel_loc.assign((size_t)m, 0);
+  int n_glob = 0;
+  for (size_t q = 0; q < bs.size(); ++q) {
+    const int j = bs[q];
+    const bool sel = !select || select[j] || (bz[q] == 2 && select[j + 1]);
+    if (!sel) continue;
+    const int own = (j / kShardNB) % P;
+    for (int k = 0; k < bz[q]; ++k) cols[own].push_back(ShardCol{n_glob + k, j + bz[q] - 1});
+    if (own == p)
+      for (int k = 0; k < bz[q]; ++k) sel_loc[j + k] = 1;
+    n_glob += bz[q];
+  }
+}
+
+int tgevc_sharded(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
+                  const int* select, double* X, long long ldx, int* cse, const double* Sh = nullptr,
+                  long long ldsh = 0, const double* Th = nullptr, long long ldth = 0) {
+  cudaStream_t st = c->stream;
+  const NcclApi* api = c->comm ? nccl_api() : nullptr;
+  if (c->comm && !api) return ZZ_ERR_NCCL;
+  const int P = (c->nranks > 1) ? c->nranks : c->shard_P;
+  const int p = (c->nranks > 1) ? c->rank : c->shard_p;
+  const bool root = c->rank == 0;               // communication role
+  const bool recv_role = c->comm && (!root || p != 0);   // computes from the broadcast copy
+  // ---- a1 on rank 0, the subdiagonal to every rank ----
+  std::vector<double> sub((size_t)std::max(m - 1, 1), 0.0);
+  if (m > 1) {
+    CK(c->subd.ensure(sizeof(double) * (size_t)m));
+    double* sd = c->subd.as<double>();
+    if (root) {
+      if (Sh) {
+        for (int j = 0; j + 1 < m; ++j) sub[j] = Sh[(size_t)j * ldsh + j + 1];
+        CK(cudaMemcpyAsync(sd, sub.data(), sizeof(double) * (m - 1), cudaMemcpyHostToDevice, st));
+      } else {
+        CK(launch_subdiag(S, lds, m, sd, st));
+      }
+    }
+    if (c->comm && api->broadcast(sd, sd, (size_t)(m - 1), ncclFloat64, 0, c->comm, st) != ncclSuccess)
+      return ZZ_ERR_NCCL;
+    CK(cudaMemcpyAsync(sub.data(), sd, sizeof(double) * (m - 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  std::vector<int> bs, bz;
+  const int nb = blocks_host(m, sub.data(), bs, bz);
+  if (nb < 0) return nb;
+  // ---- ownership: global columns of every shard (block order), the local select ----
+  std::vector<std::vector<ShardCol>> cols;
+  std::vector<int> sel_loc;
+  shard_owners(m, bs, bz, select, P, p, cols, sel_loc);
+  const int n_loc = (int)cols[p].size();
+  // ---- the local solve: all of S, T's panels stream in; own columns only ----
+  const long long ldl = (m + 1) & ~1LL;
+  CK(c->Xloc.ensure(sizeof(double) * (size_t)ldl * std::max(n_loc, 1)));
+  CK(c->Eloc.ensure(sizeof(int) * (size_t)std::max(n_loc, 1)));
+  const double* Sc = S;
+  const double* Tc = T;
+  long long ldsc = lds, ldtc = ldt;
+  if (recv_role) {
+    CK(c->Sw.ensure(sizeof(double) * (size_t)ldl * m));
+    CK(c->Tw.ensure(sizeof(double) * (size_t)ldl * m));
+    Sc = c->Sw.as<double>();
+    Tc = c->Tw.as<double>();
+    ldsc = ldtc = ldl;
+  }
+  int r;
+  if (c->comm || Sh) {
+    size_t pan = 0;   // largest panel pair: 2 x (rows up to the subdiagonal) x mb
+    const int mbt = tile_of(c->mb);
+    pan = 2 * (size_t)(m + 1) * (size_t)std::min(mbt, m);
+    if (c->comm) CK(c->bbuf.ensure(sizeof(double) * pan));
+    if (!c->copy) CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    if (!c->e_copy) CK(cudaEventCreateWithFlags(&c->e_copy, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->e_copy, st));
+    CK(cudaStreamWaitEvent(c->copy, c->e_copy, 0));
+    Feed fd;
+    fd.Sh = Sh; fd.ldsh = ldsh; fd.Th = Th; fd.ldth = ldth;
+    fd.sub = sub.data();
+    fd.copy = c->copy;
+    fd.ev = &c->ev_copy;
+    fd.comm = c->comm;
+    fd.api = api;
+    fd.root = root;
+    fd.Ssrc = S; fd.ldss = lds; fd.Tsrc = T; fd.ldts = ldt;
+    fd.bbuf = c->bbuf.as<double>();
+    fd.wait = recv_role || Sh != nullptr;
+    r = tgevc_device(c, m, Sc, ldsc, Tc, ldtc, sel_loc.data(), c->Xloc.as<double>(), ldl, c->Eloc.as<int>(), &fd);
+  } else {
+    r = tgevc_device(c, m, Sc, ldsc, Tc, ldtc, sel_loc.data(), c->Xloc.as<double>(), ldl, c->Eloc.as<int>());
+  }
+  if (r) return r;
+  // ---- gather: pack the upper parts (rows 0 .. r_c) of the local columns ----
+  auto region = [&](int q, std::vector<long long>* off) -> long long {   // bytes of shard q's buffer
+    long long o = 0;
+    if (off) off->resize(cols[q].size());
+    for (size_t l = 0; l < cols[q].size(); ++l) {
+      if (off) (*off)[l] = o;
+      o += cols[q][l].r + 1;
+    }
+    return ((8 * o + 4 * (long long)cols[q].size()) + 15) / 16 * 16;
+  };
+  // rank 0 unpacks every shard (nranks > 1) or the emulated shard p (one GPU)
+  auto unpacked = [&](int q) { return root && (c->nranks > 1 || q == p); };
+  std::vector<long long> rbase((size_t)P + 1, 0);
+  for (int q = 0; q < P; ++q) rbase[q + 1] = rbase[q] + (unpacked(q) ? region(q, nullptr) : 0);
+  std::vector<long long> loff;
+  const long long my_bytes = region(p, &loff);
+  long long dsum = 0;
+  for (int l = 0; l < n_loc; ++l) dsum += cols[p][l].r + 1;
+  // pack destination: rank 0's own shard goes straight into its receive region
+  const bool self_pack = root && !(c->comm && p != 0);
+  CK(c->recvb.ensure((size_t)std::max(rbase[P], (long long)16)));
+  if (!self_pack) CK(c->sendb.ensure((size_t)std::max(my_bytes, (long long)16)));
+  unsigned char* pk = self_pack ? c->recvb.as<unsigned char>() + rbase[p] : c->sendb.as<unsigned char>();
+  {
+    // tables: [off (int64) | h (int32)]
+    std::vector<long long> tb((size_t)n_loc * 2);
+    for (int l = 0; l < n_loc; ++l) { tb[l] = loff[l]; reinterpret_cast<int*>(tb.data() + n_loc)[l] = cols[p][l].r + 1; }
+    CK(c->gtab.ensure(sizeof(long long) * 2 * (size_t)std::max(n_loc, 1) + 16));
+    if (n_loc > 0) CK(cudaMemcpyAsync(c->gtab.p, tb.data(), sizeof(long long) * 2 * n_loc, cudaMemcpyHostToDevice, st));
+    CK(launch_shard_pack(c->Xloc.as<double>(), ldl, c->Eloc.as<int>(), n_loc, c->gtab.as<long long>(),
+                         reinterpret_cast<const int*>(c->gtab.as<long long>() + n_loc),
+                         reinterpret_cast<double*>(pk), reinterpret_cast<int*>(pk + 8 * dsum), st));
+    CK(cudaStreamSynchronize(st));   // the tables are host vectors
+  }
+  if (c->comm) {
+    if (api->groupStart() != ncclSuccess) return ZZ_ERR_NCCL;
+    bool ok = true;
+    if (!self_pack) ok &= api->send(pk, (size_t)my_bytes, ncclUint8, 0, c->comm, st) == ncclSuccess;
+    if (root) {
+      for (int q = 0; q < P; ++q) {
+        if (!unpacked(q) || (q == p && self_pack)) continue;
+        const int src = (c->nranks > 1) ? q : 0;
+        ok &= api->recv(c->recvb.as<unsigned char>() + rbase[q], (size_t)(rbase[q + 1] - rbase[q]), ncclUint8, src,
+                        c->comm, st) == ncclSuccess;
+      }
+    }
+    if (api->groupEnd() != ncclSuccess || !ok) return ZZ_ERR_NCCL;
+  }
+  // ---- rank 0: every received column into its global position of X ----
+  if (root) {
+    std::vector<long long> bo, beo;
+    std::vector<int> hh, gg;
+    for (int q = 0; q < P; ++q) {
+      if (!unpacked(q)) continue;
+      std::vector<long long> off;
+      region(q, &off);
+      long long ds = 0;
+      for (const ShardCol& sc : cols[q]) ds += sc.r + 1;
+      for (size_t l = 0; l < cols[q].size(); ++l) {
+        bo.push_back(rbase[q] + 8 * off[l]);
+        beo.push_back(rbase[q] + 8 * ds + 4 * (long long)l);
+        hh.push_back(cols[q][l].r + 1);
+        gg.push_back(cols[q][l].g);
+      }
+    }
+    const int ne = (int)gg.size();
+    CK(c->gtab.ensure((sizeof(long long) * 2 + sizeof(int) * 2) * (size_t)std::max(ne, 1) + 16));
+    long long* tb = c->gtab.as<long long>();
+    if (ne > 0) {
+      CK(cudaMemcpyAsync(tb, bo.data(), sizeof(long long) * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(tb + ne, beo.data(), sizeof(long long) * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(tb + 2 * ne, hh.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(reinterpret_cast<int*>(tb + 2 * ne) + ne, gg.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+    }
+    CK(launch_shard_unpack(c->recvb.as<unsigned char>(), ne, tb, tb + ne, reinterpret_cast<const int*>(tb + 2 * ne),
+                           reinterpret_cast<const int*>(tb + 2 * ne) + ne, m, X, ldx, cse, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    CK(cudaStreamSynchronize(st));
+  }
+  c->info.n_sel = n_loc;
+  c->info.d_logmax = c->info.d_a = c->info.d_b = c->info.d_beta = nullptr;   // local columns only
   return 0;
 }
 
@@ -940,11 +1202,24 @@ int ctx_acquire(cudaStream_t* st, cublasHandle_t* blas, int* mb, zz_info_t** inf
 
 extern "C" {
 
-int zz_init(int device) {
+int zz_get_unique_id(unsigned char* id) {
+  if (!id) return -1;
+  const NcclApi* api = nccl_api();
+  if (!api) return ZZ_ERR_NCCL;
+  ncclUniqueId u;
+  if (api->getUniqueId(&u) != ncclSuccess) return ZZ_ERR_NCCL;
+  memcpy(id, u.internal, sizeof(u.internal));
+  return 0;
+}
+
+int zz_init(int device, int nranks, int rank, const unsigned char* id) {
+  if (nranks < 1) return -2;
+  if (rank < 0 || rank >= nranks) return -3;
+  if (nranks > 1 && !id) return -4;
   int nd = 0;
   if (cudaGetDeviceCount(&nd) != cudaSuccess || device < 0 || device >= nd) return ZZ_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return ZZ_ERR_CUDA;
-  if (g_ctx && g_ctx->device != device) {
+  if (g_ctx && (g_ctx->device != device || g_ctx->comm || id)) {
     g_ctx->release();
     delete g_ctx;
     g_ctx = nullptr;
@@ -954,6 +1229,30 @@ int zz_init(int device) {
     memset(&g_ctx->info, 0, sizeof(g_ctx->info));
   }
   g_ctx->device = device;
+  g_ctx->nranks = nranks;
+  g_ctx->rank = rank;
+  g_ctx->shard_p = 0;
+  g_ctx->shard_P = 1;
+  if (id) {
+    const NcclApi* api = nccl_api();
+    if (!api) return ZZ_ERR_NCCL;
+    ncclUniqueId u;
+    memcpy(u.internal, id, sizeof(u.internal));
+    if (api->commInitRank(&g_ctx->comm, nranks, u, rank) != ncclSuccess) {
+      g_ctx->comm = nullptr;
+      return ZZ_ERR_NCCL;
+    }
+  }
+  return 0;
+}
+
+int zz_set_shard(int p, int P) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (P < 1 || P > 4096) return -2;
+  if (p < 0 || p >= P) return -1;
+  if (g_ctx->nranks > 1) return ZZ_ERR_SHARD;
+  g_ctx->shard_p = p;
+  g_ctx->shard_P = P;
   return 0;
 }
 
@@ -992,15 +1291,20 @@ int zz_set_timing(int on) {
 
 int zz_tgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,
              int ldx, int* col_scale_exp) {
-  int a = check_args(m, S, lds, T, ldt, X, ldx);
+  Context* c = g_ctx;
+  // collective call: only rank 0 passes S, T, X (the other ranks' pointers are ignored)
+  const bool nonroot = c && c->nranks > 1 && c->rank != 0;
+  int a = nonroot ? (m < 0 ? -1 : 0) : check_args(m, S, lds, T, ldt, X, ldx);
   if (a) return a;
-  if (!g_ctx) return ZZ_ERR_NOCTX;
-  if (cudaSetDevice(g_ctx->device) != cudaSuccess) return ZZ_ERR_CUDA;
+  if (!c) return ZZ_ERR_NOCTX;
+  if (cudaSetDevice(c->device) != cudaSuccess) return ZZ_ERR_CUDA;
   if (m == 0) {
-    memset(&g_ctx->info, 0, sizeof(g_ctx->info));
+    memset(&c->info, 0, sizeof(c->info));
     return 0;
   }
-  return tgevc_device(g_ctx, m, S, lds, T, ldt, select, X, ldx, col_scale_exp);
+  if (c->nranks > 1 || c->shard_P > 1 || c->comm)
+    return tgevc_sharded(c, m, S, lds, T, ldt, select, X, ldx, col_scale_exp);
+  return tgevc_device(c, m, S, lds, T, ldt, select, X, ldx, col_scale_exp);
 }
 
 int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, const int* select,
@@ -1034,12 +1338,16 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
 
 int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, const int* select, double* X,
                   int ldx, int* col_scale_exp) {
-  int a = check_args(m, S, lds, T, ldt, X, ldx);
-  if (a) return a;
-  if (!g_ctx) return ZZ_ERR_NOCTX;
   Context* c = g_ctx;
+  const bool nonroot = c && c->nranks > 1 && c->rank != 0;
+  int a = nonroot ? (m < 0 ? -1 : 0) : check_args(m, S, lds, T, ldt, X, ldx);
+  if (a) return a;
+  if (!c) return ZZ_ERR_NOCTX;
   if (cudaSetDevice(c->device) != cudaSuccess) return ZZ_ERR_CUDA;
   if (m == 0) return 0;
+  const bool coll = c->nranks > 1 || c->comm;
+  if (c->shard_P > 1) return ZZ_ERR_SHARD;     // the one-GPU shard emulation is device-only
+  if (nonroot) return tgevc_sharded(c, m, nullptr, 0, nullptr, 0, select, nullptr, 0, nullptr);
   int n_sel = zz_count_columns(m, S, lds, select);
   if (n_sel < 0) return n_sel;
   cudaStream_t st = c->stream;
@@ -1053,8 +1361,9 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
   if (!c->e_copy) CK(cudaEventCreateWithFlags(&c->e_copy, cudaEventDisableTiming));
   CK(cudaEventRecord(c->e_copy, st));
   CK(cudaStreamWaitEvent(c->copy, c->e_copy, 0));
-  HostStage hs;
+  Feed hs;
   hs.Sh = S; hs.ldsh = lds; hs.Th = T; hs.ldth = ldt; hs.copy = c->copy; hs.ev = &c->ev_copy;
+  hs.Ssrc = c->hS.as<double>(); hs.ldss = ld; hs.Tsrc = c->hT.as<double>(); hs.ldts = ld;
   // X is block-upper-triangular: column c is zero below its last row r_c.  Only the upper
   // part travels back over PCIe (one 2D copy per 64-column block, rows 0 .. the block's
   // largest r_c); the zeros below are written by host threads while the GPU solves (the
@@ -1082,8 +1391,10 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
           memset(X + (size_t)cc * ldx + r0, 0, sizeof(double) * (size_t)(m - r0));
       }
     });
-  int r = tgevc_device(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
-                       c->hE.as<int>(), &hs);
+  int r = coll ? tgevc_sharded(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
+                               c->hE.as<int>(), S, lds, T, ldt)
+               : tgevc_device(c, m, c->hS.as<double>(), ld, c->hT.as<double>(), ld, select, c->hX.as<double>(), ld,
+                              c->hE.as<int>(), &hs);
   for (auto& th : zt) th.join();
   if (r) return r;
   if (n_sel > 0) {
@@ -1131,6 +1442,26 @@ int zz_partition(int m, const double* sub, int mb, int* tile_start) {
   return M;
 }
 
+int zz_shard_columns(int m, const double* sub, const int* select, int P, int p, int* cols) {
+  if (m < 0) return -1;
+  if (P < 1) return -4;
+  if (p < 0 || p >= P) return -5;
+  std::vector<double> s((size_t)std::max(m, 1), 0.0);
+  if (m > 1) {
+    if (!sub) return -2;
+    memcpy(s.data(), sub, sizeof(double) * (m - 1));
+  }
+  std::vector<int> bs, bz;
+  const int nb = blocks_host(m, s.data(), bs, bz);
+  if (nb < 0) return nb;
+  std::vector<std::vector<ShardCol>> own;
+  std::vector<int> sel_loc;
+  shard_owners(m, bs, bz, select, P, p, own, sel_loc);
+  if (cols)
+    for (size_t l = 0; l < own[p].size(); ++l) cols[l] = own[p][l].g;
+  return (int)own[p].size();
+}
+
 int zz_last_info(zz_info_t* out) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (out) *out = g_ctx->info;
@@ -1157,6 +1488,8 @@ const char* zz_status_string(int s) {
     case ZZ_ERR_OVERLAP: return "overlapping 2x2 blocks (two consecutive nonzero subdiagonals)";
     case ZZ_ERR_TILE: return "unsupported tile size";
     case ZZ_ERR_CPLXDIAG: return "a diagonal entry of T is not real (zz_ztgevc)";
+    case ZZ_ERR_NCCL: return "NCCL error (or NCCL not available)";
+    case ZZ_ERR_SHARD: return "zz_set_shard: not with a multi-rank context / not for this call";
     default: return (s >= -9) ? "invalid argument" : "unknown status";
   }
 }

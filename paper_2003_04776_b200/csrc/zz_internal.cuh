@@ -7,6 +7,8 @@
 
 #include <algorithm>
 
+#include <nccl.h>
+
 namespace zz {
 
 // ------------------------------------------------------------------------------------
@@ -58,6 +60,7 @@ struct DevPlan {
   double* col_a;
   double* col_b;
   double* col_beta;
+  double* logmax;     // L_c = log2(max measure of the stored column before normalisation) - e_c
   int* col_kind;
   int* col_r;         // last row of the column's diagonal block
   int* col_tile;      // tile index of that block
@@ -209,5 +212,26 @@ cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const i
 cudaError_t launch_flip_transpose(const double* A, long long lda, double* B, long long ldb, int m, cudaStream_t st);
 cudaError_t launch_left_gather(const double* Xf, long long ldxf, double* Y, long long ldy, int m, int n_sel,
                                const int* kind_f, const int* ef, int* ey, cudaStream_t st);
+
+// zz_comm.cu: NCCL (dlopen'ed at first use; nullptr if unavailable) and the gather kernels
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*);
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*commDestroy)(ncclComm_t);
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*groupStart)();
+  ncclResult_t (*groupEnd)();
+};
+const NcclApi* nccl_api();
+// eigenvalue blocks are owned in groups of kShardNB rows, cyclically over the ranks
+// (block of first row j -> shard (j / kShardNB) mod P)
+constexpr int kShardNB = 64;
+cudaError_t launch_shard_pack(const double* X, long long ldx, const int* cse, int n, const long long* off,
+                              const int* h, double* buf, int* ebuf, cudaStream_t st);
+cudaError_t launch_shard_unpack(const unsigned char* buf, int ne, const long long* boff, const long long* beoff,
+                                const int* h, const int* g, int m, double* X, long long ldx, int* cse,
+                                cudaStream_t st);
 
 }  // namespace zz

@@ -705,6 +705,9 @@ __global__ void k_col_final(int n_sel, int M, DevPlan P, int* col_scale_exp, int
   double rec = (h > 0.0) ? __ddiv_rn(0.5, h) : 1.0;
   exp_tmp[c] = ec;
   rec_tmp[c] = rec;
+  // L_c of SURVEY.md s.8(c) O9: h is half the LAPACK measure (|x| or |x|+|y|) of the column
+  // at exponent e_c, so log2(2h) - e_c is the log2 of the tip-normalised vector's maximum
+  P.logmax[c] = (h > 0.0) ? log2(h) + 1.0 - (double)ec : -INFINITY;
   if (col_scale_exp) col_scale_exp[c] = ec;
   if (ec < 0) {
     atomicAdd(&stats[0], 1);

@@ -82,7 +82,13 @@ def test_no_cpu_fallback():
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    assert zz.load().zz_init(0) == -100
+    assert zz.load().zz_init(0, 1, 0, None) == -100
+    # multi-rank arguments are validated before any device or NCCL access
+    lib = zz.load()
+    assert lib.zz_init(0, 0, 0, None) == -2
+    assert lib.zz_init(0, 2, 2, None) == -3
+    assert lib.zz_init(0, 2, 1, None) == -4
+    assert lib.zz_set_shard(0, 2) == -103
     S = torch.eye(4, dtype=torch.float64)
     with pytest.raises(ValueError):
         zz.tgevc(S, S)
