@@ -58,18 +58,18 @@ struct Context {
   cudaStream_t stream = nullptr;
   int mb = 0;
   int timing = 0;
-  // step groups of the wavefront: 1 (none), 2 (pairs) or 3 (triples); zz_set_fusion, ZZ_FUSE
-  int fusion = getenv("ZZ_FUSE") ? atoi(getenv("ZZ_FUSE")) : 4;
-  // lookahead (ZZ_LOOKAHEAD): the chain of solves runs on a high-priority stream beside the
-  // bulk of the previous group's update (DESIGN.md s.6 "Lookahead")
-  int lookahead = getenv("ZZ_LOOKAHEAD") ? atoi(getenv("ZZ_LOOKAHEAD")) : 1;
+  // step groups of the wavefront: k consecutive steps share one update (zz_set_fusion)
+  int fusion = 4;
+  // lookahead (zz_set_lookahead): the chain of solves runs on a high-priority stream beside
+  // the bulk of the previous group's update (DESIGN.md s.6 "Lookahead"); 1 = automatic
+  int lookahead = 1;
   cudaStream_t hi = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::vector<cudaEvent_t> ev_la;
   zz_info_t info;
   EncodeTiledFn encode = nullptr;
   // workspace
-  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Apk, Xi, egrp;
+  Buf sub, colf, coli, items, tiles, rows, blks, state, seg, norms, W, status, tmp, Sc, Tc, Xi, egrp;
   Buf Wx[kMaxGroup - 1];   // the W operands of a step group's later steps
   Buf Wy[kMaxGroup];       // second set (lookahead: groups alternate between the sets)
   Buf sYb, nYb;            // second sY set; per-column bound of the pending rows (lookahead)
@@ -91,7 +91,7 @@ struct Context {
   ~Context() {}
   void release() {
     Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
-                  &status, &tmp, &Sc, &Tc, &Apk, &Xi, &egrp, &hS, &hT, &hX, &hE};
+                  &status, &tmp, &Sc, &Tc, &Xi, &egrp, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
     for (Buf& b : Wx) b.release();
     for (Buf& b : Wy) b.release();
@@ -194,7 +194,7 @@ int make_map(Context* c, CUtensorMap* tm, const double* A, long long lda, int m)
   }
   cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)m};
   cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
-  cuuint32_t box[2] = {(cuuint32_t)update_box_rows(), (cuuint32_t)kBK};
+  cuuint32_t box[2] = {8u, (cuuint32_t)kBK};   // 8 rows x 16 columns per TMA box
   cuuint32_t estr[2] = {1, 1};
   CUresult r = c->encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -315,9 +315,8 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     rbeg[I] = (int)(std::lower_bound(real_tile.begin(), real_tile.end(), I) - real_tile.begin());
     pbeg[I] = (int)(std::lower_bound(pair_tile.begin(), pair_tile.end(), I) - pair_tile.begin());
   }
-  // diagonal-solve kernel: 3 = 8 columns per warp with DMMA in-tile updates (default, tiles
-  // of <= 128 rows), 1 = warp per eigenvector (any tile; used above 128 rows)
-  static const int diag_kind = getenv("ZZ_DIAG") ? atoi(getenv("ZZ_DIAG")) : 3;
+  // diagonal-solve kernel: k_diag3 (8 columns per warp, DMMA in-tile updates) for tiles of
+  // <= 128 rows, k_diag (warp per eigenvector) above
   // ---- workspace ----
   const int n = std::max(n_sel, 1);
   const int nks_max = ceil_div(mb, kBK);
@@ -548,7 +547,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   // contraction with K = [tile J | tile I] (twice the K of a single step: half the C-tile
   // traffic and prologue/epilogue per flop).
   const int fusion = std::max(1, std::min(kMaxGroup, c->fusion));
-  const bool can_fuse = fusion > 1 && diag_kind != 1 && vec && update_version() == 2 && mb <= kDiag2MaxNT;
+  const bool can_fuse = fusion > 1 && vec && mb <= kDiag2MaxNT;
   for (int k = 0; k + 1 < fusion; ++k) CK(c->Wx[k].ensure(c->W.cap));
   // Lookahead: the chain of solves and band updates runs on a high-priority stream `ms`; the
   // bulk of each group's update (the rows above the next group's band) runs on the caller's
@@ -586,16 +585,6 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   bool prev_bound = false;           // the previous group recorded nYb (lookahead)
   cudaEvent_t ev_rest = nullptr;     // the bulk update of the previous group (lookahead)
   int nyb = (M - 1) & 1;   // nY buffer holding the pending max for the next decision
-  static const bool dbg_sync = getenv("ZZ_DEBUG_SYNC") != nullptr;
-  auto dbg = [&](const char* what, int I) -> int {
-    if (!dbg_sync) return 0;
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-      fprintf(stderr, "zz: %s at step %d failed: %s\n", what, I, cudaGetErrorString(e));
-      return map_err(e);
-    }
-    return 0;
-  };
   auto panel_ready = [&](int I) -> int {
     if (!hs) return 0;
     // panel I has arrived: its eigenvalue pairs and column-panel norms
@@ -620,7 +609,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     dp.X = X; dp.ldx = ldx;
     dp.P = P;
     dp.nY_in = nyb;
-    if (dp.nt <= kDiag2MaxNT && diag_kind != 1) {
+    if (dp.nt <= kDiag2MaxNT) {
       Diag2Params d2;
       memset(&d2, 0, sizeof(d2));
       d2.I = I; d2.t0 = dp.t0; d2.nt = dp.nt;
@@ -636,8 +625,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.X = X; d2.ldx = ldx;
       d2.P = P;
       d2.P.sY = sY_set[gpar];
-      static const int la_pack = getenv("ZZ_LA_PACK") ? atoi(getenv("ZZ_LA_PACK")) : 1;
-      d2.pack = la && la_pack;
+      d2.pack = la;
       d2.nY_in = dp.nY_in;
       d2.Wout = Wout;
       d2.grp_slot = -1;
@@ -664,13 +652,12 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       CK(launch_diag(dp, ms));
     }
     launches++;
-    return dbg(fuse_from && fuse_from->fused ? "diag (fused)" : "diag", I);
+    return 0;
   };
   auto update = [&](UpdParams up, int n_m, cudaStream_t us) -> int {
     const int n_n = ceil_div(n_sel, kBN) - up.ntile0;
     if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd], us));
     CK(launch_update(&tmS, &tmT, up, n_m, n_n, us));
-    if (int r = dbg(up.nxs ? "fused update" : (up.row_lo ? "thin update" : "update"), up.t0 / std::max(mb, 1))) return r;
     if (c->timing) CK(cudaEventRecord(c->ev[2 * n_upd + 1], us));
     n_upd++;
     launches++;
@@ -709,7 +696,6 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       len = fusion - (M - 1 - I) % fusion;
       while (len > 1 && I - (len - 1) < 1) --len;
     }
-    const int J = I - 1, K = I - 2;
     auto nks_of = [&](int t) { return ceil_div(ts[t + 1] - ts[t], kBK); };
     if (len >= 2) {
       // ---- a step group (I, I-1, ..., L = I-len+1): diag of each step, thin updates of the
@@ -822,12 +808,6 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     if ((r = diag(I, P.W, nullptr))) return r;
     if (I > 0) {
       UpdParams up = base_up(I);
-      if (update_packs()) {
-        CK(c->Apk.ensure(pack_bytes(ts[I], up.nks)));
-        CK(launch_pack(Su, ldsu, Tu, ldtu, ts[I], ts[I], ts[I + 1] - ts[I], up.nks, c->Apk.as<double>(), st));
-        up.Apk = c->Apk.as<double>();
-        launches++;
-      }
       if ((r = update(up, ceil_div(ts[I], kBM), ms))) return r;
       nyb = 1 - nyb;
     }

@@ -127,15 +127,12 @@ struct UpdParams {
   const int* sY;
   unsigned long long* nY_out;
   int vec;           // 16-byte aligned X access possible
-  const double* Apk; // S/T panel packed in fragment order (update_packs()), or null
   int row_lo;        // rows [row_lo, rows) are updated (0, or a tile start for the thin update)
   // further K segments of a step group's update (MODE 1): S/T columns of tile xt0[e]
   // (xnks[e] chunks per part) against xW[e], in this order after (t0, nks, W)
   int nxs;
   int xt0[kMaxGroup - 1], xnks[kMaxGroup - 1];
   const double* xW[kMaxGroup - 1];
-  int l2hint;        // L2 eviction priorities: C evict_first, W evict_last (set by launch_update)
-  int ngroup;        // N tiles per group of the CTA order (set by launch_update)
 };
 
 // Diagonal solve with 8 columns per warp (zz_diag3.cu): tiles of at most kDiag2MaxNT rows.
@@ -198,14 +195,6 @@ cudaError_t launch_normalize(int m, int n_sel, int M, double* X, long long ldx, 
 cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const UpdParams& p,
                           int n_mtiles, int n_ntiles, cudaStream_t st);
 size_t diag_smem_bytes(int nt);
-int update_version();
-// The S/T panel of a step packed in the DMMA fragment order of the update kernel:
-// [m-tile][k-chunk][8-row group][k/4][row in group][k%4], one 16 KB block per stage.
-bool update_packs();
-size_t pack_bytes(int rows, int nks);
-cudaError_t launch_pack(const double* S, long long lds, const double* T, long long ldt, int rows, int t0, int nt,
-                        int nks, double* Apk, cudaStream_t st);
-int update_box_rows();   // rows per TMA box of the S/T tensor maps
 // zz_back.cu: LAPACK normalisation of the back-transformed columns (xTGEVC HOWMNY='B')
 cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const int* col_kind, cudaStream_t st);
 // zz_left.cu: left eigenvectors through the flipped pencil S' = J S^T J, T' = J T^T J

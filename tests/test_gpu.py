@@ -189,26 +189,6 @@ def test_select_subsets_bitwise(zz):
     assert Xs.shape == (m, 0) and info["n_sel"] == 0
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_sharded_columns_bitwise(zz, P):
-    """the multi-GPU shard (cyclic column blocks, paper_2003_04776_b200/dist.py) computes each
-    rank's columns with select; assembled, X equals the 1-GPU X bitwise (per-column arithmetic
-    is independent of the other columns)."""
-    from paper_2003_04776_b200 import dist as zdist
-    S, T, _ = gen.config("C2", seed=2)
-    m = S.shape[0]
-    Xf, ef, _ = solve(zz, S, T, mb=128)
-    sub = np.diagonal(S, -1)
-    Xa = np.full_like(Xf, np.nan)
-    Ea = np.zeros_like(ef)
-    for r in range(P):
-        sel, cols = zdist.shard_select(sub, m, r, P, nb=64)
-        Xr, er, _ = solve(zz, S, T, mb=128, select=sel)
-        Xa[:, cols] = Xr
-        Ea[cols] = er
-    assert np.array_equal(Xa, Xf) and np.array_equal(Ea, ef)
-
-
 def test_leading_dimensions_and_alignment(zz):
     S, T, _ = gen.config("C2", seed=0, m=700, n2=105)
     X0, e0, _ = solve(zz, S, T, mb=64)
