@@ -75,6 +75,7 @@ struct Context {
   Buf sYb, nYb;            // second sY set; per-column bound of the pending rows (lookahead)
   Buf hS, hT, hX, hE;  // device staging of zz_tgevc_host
   Buf Xb;              // X of zz_tgevc_back / the flipped solve of zz_tgevc_left
+  Buf Xp, btab, Vc;    // zz_tgevc_back: tile-packed X, tile tables + column maxima, aligned V
   // communicator (zz_init with an id) and the shard of this rank
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -104,6 +105,9 @@ struct Context {
     if (hi) cudaStreamDestroy(hi);
     hi = nullptr;
     Xb.release();
+    Xp.release();
+    btab.release();
+    Vc.release();
     Buf* cb[] = {&Sw, &Tw, &Xloc, &Eloc, &bbuf, &sendb, &recvb, &gtab, &subd};
     for (Buf* b : cb) b->release();
     if (comm) {
@@ -885,9 +889,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   return 0;
 }
 
-// xTGEVC HOWMNY='B' (reading A1): W = V X, column block by column block with
-// K = 1 + the block's largest r_c (columns are in block order, so r_c is non-decreasing and
-// X is zero below r_c), then LAPACK's normalisation of the back-transformed columns.
+// xTGEVC HOWMNY='B' (reading A1): W = V X as one FP64 tensor-core
+// contraction over the triangular K range (columns are in block order, so r_c is
+// non-decreasing and X is zero below r_c: tile J of 64 columns needs K_J = 1 + its last
+// column's r_c), then LAPACK's normalisation of the back-transformed columns (zz_back.cu).
 int tgevc_back_device(Context* c, int m, const double* S, long long lds, const double* T, long long ldt,
                       const int* select, const double* V, long long ldv, double* W, long long ldw, int* cse) {
   cudaStream_t st = c->stream;
@@ -898,27 +903,59 @@ int tgevc_back_device(Context* c, int m, const double* S, long long lds, const d
   if (r) return r;
   const int n_sel = c->info.n_sel;
   if (n_sel == 0) return 0;
-  if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
-  if (cublasSetStream(c->blas, st) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
-  if (cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
   CK(cudaEventRecord(c->e0, st));
-  const double one = 1.0, zero = 0.0;
-  const int nbk = 256;
-  for (int c0 = 0; c0 < n_sel; c0 += nbk) {
-    const int nc = std::min(nbk, n_sel - c0);
-    const int K = c->last_col_r[c0 + nc - 1] + 1;
-    if (cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m, nc, K, &one, V, (int)ldv, Xb + (size_t)c0 * ldxb,
-                    (int)ldxb, &zero, W + (size_t)c0 * ldw, (int)ldw) != CUBLAS_STATUS_SUCCESS)
-      return ZZ_ERR_CUDA;
+  // V by TMA needs a 16-byte aligned base and an even leading dimension; W is stored with
+  // 16-byte stores: otherwise through aligned library copies
+  const double* Vu = V;
+  long long ldvu = ldv;
+  if ((ldv & 1) || !aligned16(V)) {
+    CK(c->Vc.ensure(sizeof(double) * (size_t)ldxb * m));
+    CK(cudaMemcpy2DAsync(c->Vc.p, sizeof(double) * ldxb, V, sizeof(double) * ldv, sizeof(double) * m, m,
+                         cudaMemcpyDeviceToDevice, st));
+    Vu = c->Vc.as<double>();
+    ldvu = ldxb;
   }
+  double* Wu = W;
+  long long ldwu = ldw;
+  if ((ldw & 1) || !aligned16(W)) {
+    CK(c->Xi.ensure(sizeof(double) * (size_t)ldxb * n_sel));
+    Wu = c->Xi.as<double>();
+    ldwu = ldxb;
+  }
+  const int n_nt = (n_sel + kBN - 1) / kBN;
+  std::vector<int> nkc((size_t)n_nt);
+  std::vector<long long> woff((size_t)n_nt);
+  long long tot = 0;
+  int max_nkc = 1;
+  for (int J = 0; J < n_nt; ++J) {
+    const int last = std::min(n_sel - 1, J * kBN + kBN - 1);
+    nkc[J] = ceil_div(c->last_col_r[last] + 1, kBK);
+    max_nkc = std::max(max_nkc, nkc[J]);
+    woff[J] = tot;
+    tot += (long long)nkc[J] * (kBN * kBK);
+  }
+  CK(c->Xp.ensure(sizeof(double) * (size_t)tot));
+  CK(c->btab.ensure((sizeof(int) + sizeof(long long)) * (size_t)n_nt + sizeof(unsigned long long) * (size_t)n_sel + 64));
+  long long* d_woff = c->btab.as<long long>();
+  int* d_nkc = reinterpret_cast<int*>(d_woff + n_nt);
+  unsigned long long* d_cmax = reinterpret_cast<unsigned long long*>(d_woff + n_nt + (n_nt + 1) / 2 + 1);
+  CK(cudaMemcpyAsync(d_woff, woff.data(), sizeof(long long) * n_nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_nkc, nkc.data(), sizeof(int) * n_nt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cmax, 0, sizeof(unsigned long long) * n_sel, st));
+  CUtensorMap tmV;
+  if (int e = make_map(c, &tmV, Vu, ldvu, m)) return e;
+  CK(launch_back_gemm(&tmV, Xb, ldxb, m, n_sel, d_nkc, d_woff, max_nkc, c->Xp.as<double>(), Wu, ldwu, d_cmax, st));
   // the column kinds of the last call are still in the workspace (DevPlan.col_kind)
-  CK(launch_back_norm(W, ldw, m, n_sel, c->coli.as<int>(), st));
+  CK(launch_back_norm(Wu, ldwu, m, n_sel, c->coli.as<int>(), d_cmax, st));
+  if (Wu != W)
+    CK(cudaMemcpy2DAsync(W, sizeof(double) * ldw, Wu, sizeof(double) * ldwu, sizeof(double) * m, n_sel,
+                         cudaMemcpyDeviceToDevice, st));
   CK(cudaEventRecord(c->e1, st));
   CK(cudaStreamSynchronize(st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->e0, c->e1);
   c->info.ms_back = ms;
-  c->info.total_launches += 1;
+  c->info.total_launches += 3;
   return 0;
 }
 

@@ -196,7 +196,11 @@ cudaError_t launch_update(const CUtensorMap* tmS, const CUtensorMap* tmT, const 
                           int n_mtiles, int n_ntiles, cudaStream_t st);
 size_t diag_smem_bytes(int nt);
 // zz_back.cu: LAPACK normalisation of the back-transformed columns (xTGEVC HOWMNY='B')
-cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const int* col_kind, cudaStream_t st);
+cudaError_t launch_back_gemm(const CUtensorMap* tmV, const double* X, long long ldx, int m, int n_sel,
+                             const int* nkc, const long long* woff, int max_nkc, double* Xp, double* W,
+                             long long ldw, unsigned long long* colmax, cudaStream_t st);
+cudaError_t launch_back_norm(double* W, long long ldw, int m, int n_sel, const int* col_kind,
+                             const unsigned long long* colmax, cudaStream_t st);
 // zz_left.cu: left eigenvectors through the flipped pencil S' = J S^T J, T' = J T^T J
 cudaError_t launch_flip_transpose(const double* A, long long lda, double* B, long long ldb, int m, cudaStream_t st);
 cudaError_t launch_left_gather(const double* Xf, long long ldxf, double* Y, long long ldy, int m, int n_sel,

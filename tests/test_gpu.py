@@ -433,11 +433,11 @@ def test_host_path_select_ld_errors_and_prescale(zz):
 
 # ---- back-transformation W = V X (xTGEVC HOWMNY='B', include/zz.h zz_tgevc_back) ----
 
-def _back(zz, S, T, V, mb=0, select=None, ldw=None):
+def _back(zz, S, T, V, mb=0, select=None, ldw=None, ldv=None):
     zz.set_tile(mb)
     m = S.shape[0]
     n = oracle.count_columns(S, select)
-    Sd, Td, Vd = to_dev(S), to_dev(T), to_dev(V)
+    Sd, Td, Vd = to_dev(S), to_dev(T), to_dev(V, ldv)
     W = None
     if ldw is not None:
         W = torch.full((max(n, 1), ldw), np.nan, dtype=torch.float64, device="cuda").t()[:m, :n]
@@ -469,6 +469,8 @@ def test_back_select_ldw_and_residual(zz):
     W0, e0, _ = _back(zz, S, T, V, mb=64)
     W1, e1, _ = _back(zz, S, T, V, mb=64, ldw=703)        # odd ldw: bitwise the same
     assert np.array_equal(W0, W1) and np.array_equal(e0, e1)
+    W2, e2, _ = _back(zz, S, T, V, mb=64, ldv=701)        # odd ldv (aligned copy of V)
+    assert np.array_equal(W0, W2) and np.array_equal(e0, e2)
     sel = np.zeros(m, np.int32)
     sel[::7] = 1
     Ws, es, _ = _back(zz, S, T, V, mb=64, select=sel)
