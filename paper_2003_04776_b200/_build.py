@@ -46,7 +46,7 @@ def build(force=False, verbose=False):
     objs = [obj for _, obj, _ in results]
     cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
     r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO + ".tmp"] + objs
-                       + ["-L" + cudalib, "-lcublas", "-ldl", "-Xlinker", "-rpath", "-Xlinker", cudalib],
+                       + ["-L" + cudalib, "-ldl", "-Xlinker", "-rpath", "-Xlinker", cudalib],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)

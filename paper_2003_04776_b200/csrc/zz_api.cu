@@ -7,7 +7,6 @@
 // row I for every active eigenvector (tips for the blocks inside tile I), then one fused
 // robust update of all rows above it.  Two host synchronisations happen before the
 // wavefront (structure, then pair/norm status); none inside it.
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -82,7 +81,6 @@ struct Context {
   int shard_p = 0, shard_P = 1;   // zz_set_shard: one-GPU emulation of a rank's share
   Buf Sw, Tw, Xloc, Eloc, bbuf, sendb, recvb, gtab, subd;
   Buf Sl, Tl, El;      // zz_tgevc_left: S' = J S^T J, T' = J T^T J, exponents
-  cublasHandle_t blas = nullptr;          // the back-transformation GEMMs
   std::vector<int> last_col_r;            // r_c of the last call's columns (host)
   std::vector<cudaEvent_t> ev;
   std::vector<cudaEvent_t> ev_copy;       // per-panel arrival events of zz_tgevc_host
@@ -117,8 +115,6 @@ struct Context {
     Sl.release();
     Tl.release();
     El.release();
-    if (blas) cublasDestroy(blas);
-    blas = nullptr;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
     for (cudaEvent_t e : ev_copy) cudaEventDestroy(e);
@@ -1201,18 +1197,15 @@ int check_args(int m, const double* S, int lds, const double* T, int ldt, double
 
 }  // namespace
 
-// Context access for the complex-pencil path (zz_complex.cu): binds the device, creates the
-// cuBLAS handle on the context's stream, and hands out the stream, tile and info record.
-int ctx_acquire(cudaStream_t* st, cublasHandle_t* blas, int* mb, zz_info_t** info) {
+// Context access for the complex-pencil path (zz_complex.cu): binds the device and hands out
+// the stream, tile and info record.
+int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info) {
   Context* c = g_ctx;
   if (!c) return ZZ_ERR_NOCTX;
   if (cudaSetDevice(c->device) != cudaSuccess) return ZZ_ERR_CUDA;
-  if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
-  if (cublasSetStream(c->blas, c->stream) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
-  if (cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) return ZZ_ERR_CUDA;
   *st = c->stream;
-  *blas = c->blas;
   *mb = c->mb;
+  *lookahead = c->lookahead;
   *info = &c->info;
   return 0;
 }

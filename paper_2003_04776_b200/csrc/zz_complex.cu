@@ -7,14 +7,13 @@
 //       PAPER.md:175-200), which also takes the per-column scaling decision of Algorithm 3
 //        and stages the scaled B operand [beta x ; -alpha x];
 //   (3) the update of every pending row above the tile as ONE complex contraction
-//       Y <- Y - [S_panel | T_panel] [sigma beta X_I ; -sigma alpha X_I]   (K = 2 nb),
-//       a cuBLAS ZGEMM3M (Gauss's three-multiplication form, R23; ZGEMM with ZZ_Z3M=0) on
-//       the DMMA pipe over a contiguous copy of the two panels;
+//       Y <- 2^sy Y + [S_panel | T_panel] [-sigma beta X_I ; sigma alpha X_I]   (K = 2 nb),
+//       k_zupdate: Gauss's three-multiplication form (R23) as three DMMA.8x8x4 contractions
+//       sharing one TMA-staged panel, with the scaling sigma_Y in its prologue;
 //   (4) consistency and normalisation (max |Re|+|Im| = 1, ZTGEVC's convention).
 // Readings R18-R21 of DESIGN.md; the pending-row maximum is carried as an upper bound
 // (R21) instead of being measured, so the update needs no epilogue.
-#include <cublas_v2.h>
-#include <cuComplex.h>
+#include <cuda.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -23,13 +22,25 @@
 
 #include "../../include/zz.h"
 #include "zz_internal.cuh"
+#include "zz_pipe.cuh"
 
-int ctx_acquire(cudaStream_t* st, cublasHandle_t* blas, int* mb, zz_info_t** info);
+int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info);
 
 namespace zz {
 namespace {
 
 constexpr int kZMaxNB = 64;        // rows per tile: two rows per lane
+// k_zupdate tiling (below)
+constexpr int kZBM = 64;        // complex rows per CTA tile
+constexpr int kZBN = 32;        // columns per CTA tile
+constexpr int kZBK = 8;         // complex panel columns per chunk
+constexpr int kZStages = 5;
+constexpr int kZABytes = 3 * kZBM * kZBK * 8;      // 12 KB: [8 row groups][3 planes][2][32]
+constexpr int kZBBytes = 3 * kZBK * kZBN * 8;      // 6 KB: [3][kZBK/4][32][4]
+constexpr int kZUThreads = 5 * 32;
+constexpr int kZUSmem = kZStages * (kZABytes + kZBBytes) + 2 * kZStages * 8;
+constexpr int kZNGroup = 64;    // N tiles per group of the CTA order
+
 constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag
 constexpr int kZErrNonfinite = 0;  // status key = 2*row + kind
 constexpr int kZErrCplxDiag = 1;
@@ -48,9 +59,9 @@ struct ZDiagParams {
   double* nYb;
   int* e_seg;        // row I of the M x n_sel array
   double* nrmh_seg;  // row I
-  double2* B;        // 2 nt x n_act, column-major (ld 2 nt)
-  int* sy;           // per column: exponent shift of the pending rows (<= 0)
-  double tau_mul;    // 2 (four-multiplication product) or 4 (Gauss 3M, R23)
+  double* W;         // update operand, k_zupdate's layout [n-tile][chunk][3 planes][2][32][4]
+  int nkS;           // chunks of 8 panel columns per part (S, then T)
+  int* sy;           // per column: exponent shift of the pending rows (<= 0), this step's set
 };
 
 __device__ __forceinline__ double zabsm(double2 z) { return fmax(fabs(z.x), fabs(z.y)); }
@@ -139,15 +150,6 @@ __global__ void k_zcolmax(const double2* __restrict__ S, long long lds, const do
   ms = warp_max(ms);
   mt = warp_max(mt);
   if (lane == 0) { cmS[k] = ms; cmT[k] = mt; }
-}
-
-// A = [S(0:r0, r0:r0+nt) | T(0:r0, r0:r0+nt)], r0 x 2nt column-major (ld r0).
-__global__ void k_zpanel(const double2* __restrict__ S, long long lds, const double2* __restrict__ T, long long ldt,
-                         int r0, int nt, double2* __restrict__ A) {
-  const int col = blockIdx.y;   // 0 .. 2nt-1
-  const double2* src = col < nt ? S + (long long)(r0 + col) * lds : T + (long long)(r0 + col - nt) * ldt;
-  double2* dst = A + (long long)col * r0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r0; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
 // Robust diagonal-tile solve + Algorithm 3's decision
@@ -285,8 +287,10 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     const int g = min(ep, e);
     const double yh = ldexp(tipc ? 0.0 : p.nYb[c], g - ep);
     const double xh = ldexp(nx, g - e);
-    const double tau = p.tau_mul * sums;
-    const int ed = protect_update(yh, tau, xh);
+    // R23 (k_zupdate): the partial sums of Im + Re accumulate from 2^sy (|Im Y| + |Re Y|) <=
+    // 2 y^ and add up to sum_k (|Ar|+|Ai|)(|Wr|+|Wi|) <= 4 sums x^: ProtectUpdate(2 y^, 4 sums, x^)
+    const double tau = 4.0 * sums;
+    const int ed = protect_update(2.0 * yh, tau, xh);
     const int en = g + ed;
     const int sy = en - ep, sx = en - e;
     __syncwarp();
@@ -294,39 +298,230 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
       p.e_pend[c] = en;
       // R21: the bound 2^ed (yh + tau xh), not a measurement; tau xh itself may exceed the
       // range when ed < 0, so that product is formed as protect_update does (scaled by 2^-1023)
-      const double bnd = ed == 0 ? yh + tau * xh
+        const double bnd = ed == 0 ? yh + tau * xh
                                  : ldexp(yh, ed) + ldexp(ldexp(tau, -512) * ldexp(xh, -511), ed + 1023);
       p.nYb[c] = bnd * (1.0 + 0x1p-40);
     }
-    if (lane == 0) p.sy[c] = sy;   // applied to the pending rows by k_zscale_pending
-    double2* Bc = p.B + (long long)w * 2 * nt;
-    const double2 x0 = zldexp(y0, sx), x1 = zldexp(y1, sx);
-    if (lane < nt) {
-      const bool z = lane > top;
-      Bc[lane] = z ? make_double2(0.0, 0.0) : make_double2(be * x0.x, be * x0.y);
-      const double2 q = zmul(al, x0);
-      Bc[nt + lane] = z ? make_double2(0.0, 0.0) : make_double2(-q.x, -q.y);
-    }
-    if (lane + 32 < nt) {
-      const bool z = lane + 32 > top;
-      Bc[lane + 32] = z ? make_double2(0.0, 0.0) : make_double2(be * x1.x, be * x1.y);
-      const double2 q = zmul(al, x1);
-      Bc[nt + lane + 32] = z ? make_double2(0.0, 0.0) : make_double2(-q.x, -q.y);
+    if (lane == 0) p.sy[c] = sy;   // applied to the pending rows in k_zupdate's prologue
+    // W(:, c) = [-sigma beta x ; sigma alpha x] in k_zupdate's stage layout, planes Re, Im and
+    // Re + Im; rows past the tile (or past a tip) are zero
+    const double2 xs[2] = {zldexp(y0, sx), zldexp(y1, sx)};
+    double* Wt = p.W + (long long)(c / kZBN) * (2 * p.nkS) * (kZBBytes / 8) + (c % kZBN) * 4;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = lane + 32 * h;
+      if (row >= 8 * p.nkS) continue;
+      const bool z = row > top;
+      const double2 ws = z ? make_double2(0.0, 0.0) : make_double2(-(be * xs[h].x), -(be * xs[h].y));
+      const double2 wt = z ? make_double2(0.0, 0.0) : zmul(al, xs[h]);
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const int kk = part ? 8 * p.nkS + row : row;
+        const double2 w = part ? wt : ws;
+        double* o = Wt + (long long)(kk / kZBK) * (kZBBytes / 8) + ((kk % kZBK) >> 2) * (kZBN * 4) + (kk & 3);
+        o[0] = w.x;
+        o[256] = w.y;
+        o[512] = __dadd_rn(w.x, w.y);
+      }
     }
   }
+  // W is read next by bulk copies (the async proxy): order the generic writes before them
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// sigma_Y of Algorithm 3: Y(0:r0, c) <- 2^sy[c] Y(0:r0, c) for the columns whose decision
-// scaled (rare); one warp per active column.  Runs on the update's stream, after the previous
-// step's update has written those rows.
-__global__ void k_zscale_pending(double2* X, long long ldx, int r0, int cs, int n_act, const int* __restrict__ sy) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= n_act) return;
-  const int c = cs + w;
-  const int k = sy[c];
-  if (k >= 0) return;
-  double2* yc = X + (long long)c * ldx;
-  for (int i = threadIdx.x & 31; i < r0; i += 32) yc[i] = zldexp(yc[i], k);
+// ------------------------------------------------------------------------------------
+// (3) The update of the pending rows as ONE complex contraction per step (PAPER.md:235's
+// composition; reading R23): Y(rows, c) <- 2^sy[c] Y + [S_panel | T_panel] W(:, c) with
+// W = [-sigma beta X_I ; sigma alpha X_I] (written by k_zdiag), by Gauss's three-multiplication
+// form on the FP64 tensor instruction (DMMA.8x8x4):
+//   T1 = Ar Wr,  T2 = Ai Wi,  T3 = (Ar + Ai)(Wr + Wi);   Re Y += T1 - T2,  Im Y += T3 - T1 - T2
+// -- three real contractions sharing one staged panel and one staged W, each in three planes
+// (Re, Im, Re + Im), 25 % fewer tensor instructions than the four-multiplication product.  The
+// accumulators start from 2^sy Re Y, 0 and 2^sy (Im Y + Re Y), so the epilogue is
+// Re = acc1 - acc2, Im = (acc3 - acc1) - acc2 (fixed order).  Bound (R23): every partial sum of
+// acc3 is <= 2 y^ + sum_k (|Ar|+|Ai|)(|Wr|+|Wi|) <= 2 y^ + 4 sums x^ -- Algorithm 3's decision
+// in k_zdiag is ProtectUpdate(2 y^, 4 sums, x^).
+//
+// k_zpack writes the panel of the step once in DMMA fragment order with its three planes
+// ([64-row tile][chunk of 8 columns][8-row group][plane][k/4][lane]), so that a stage is one
+// 12 KB bulk copy and every fragment load is one conflict-free 8-byte shared load (a TMA copy
+// of the interleaved column-major panel gives 4-way conflicts on the 16-byte (Re, Im) loads).
+// Pipeline as the real update (zz_update.cu): CTA tile 64 complex rows x 32 columns (aligned
+// 64-row tiles from row 0; rows outside [row_lo, rows) are computed but not stored), four DMMA
+// warps (32 rows x 16 columns each) and one producer warp, per stage 8 panel columns (12 KB)
+// and the matching 6 KB of W.  The contraction is computed transposed (Y^T += W^T A^T): a
+// lane's accumulators are two consecutive complex rows of one column (32-byte loads/stores).
+// ------------------------------------------------------------------------------------
+struct ZUpdParams {
+  int rows, row_lo;   // complex rows [row_lo, rows) are updated
+  int nkc;            // chunks of 8 panel columns (S part, then T part)
+  int c_begin, n_sel; // active columns
+  int ntile0;         // first 32-column tile (c_begin / 32)
+  int mtile0;         // first 64-row tile (row_lo / 64)
+  double2* X; long long ldx;
+  const double* A;    // packed panel (k_zpack)
+  const double* W;    // [n-tile][nkc][3][kZBK/4][32][4]
+  const int* sy;
+};
+
+// panel of step I in fragment order: block (mt, kc) = 64 rows x 8 columns x 3 planes, element
+// (row 8 g + cq, column 4 ks + rq, plane p) at ((g * 3 + p) * 2 + ks) * 32 + 4 cq + rq; columns
+// kc < nkS from S, then T; columns past the tile (ragged last tile) and rows >= r0 are zero
+__global__ void __launch_bounds__(256) k_zpack(const double2* __restrict__ S, long long lds,
+                                               const double2* __restrict__ T, long long ldt, int r0, int nt, int nkS,
+                                               double* __restrict__ A) {
+  __shared__ double2 tile[kZBK][kZBM + 1];
+  const int mt = blockIdx.x, kc = blockIdx.y;
+  const bool isT = kc >= nkS;
+  const double2* P = isT ? T : S;
+  const long long ld = isT ? ldt : lds;
+  const int k0 = (isT ? kc - nkS : kc) * kZBK;
+  for (int idx = threadIdx.x; idx < kZBK * kZBM; idx += blockDim.x) {
+    const int k = idx / kZBM, r = idx % kZBM;
+    const int row = mt * kZBM + r;
+    tile[k][r] = (row < r0 && k0 + k < nt) ? P[(long long)(r0 + k0 + k) * ld + row] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double* out = A + ((long long)mt * gridDim.y + kc) * (kZABytes / 8);
+  for (int o = threadIdx.x; o < kZABytes / 8; o += blockDim.x) {
+    const int ln = o & 31, ks = (o >> 5) & 1, pl = (o >> 6) % 3, g = (o >> 6) / 3;
+    const double2 v = tile[ks * 4 + (ln & 3)][g * 8 + (ln >> 2)];
+    out[o] = pl == 0 ? v.x : (pl == 1 ? v.y : __dadd_rn(v.x, v.y));
+  }
+  // read next by bulk copies (the async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_mtiles, int n_ntiles) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = reinterpret_cast<double*>(smem + kZStages * kZABytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kZStages * (kZABytes + kZBBytes));
+  uint64_t* empty = full + kZStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkc = p.nkc;
+  int mt, nt;
+  {
+    const int tile = blockIdx.x, per = n_mtiles * kZNGroup;
+    const int g = tile / per, loc = tile - g * per;
+    const int gs = min(kZNGroup, n_ntiles - g * kZNGroup);
+    mt = p.mtile0 + loc / gs;
+    nt = g * kZNGroup + loc % gs;
+  }
+  const int m0 = mt * kZBM;                       // first complex row of the tile
+  const int ntile = p.ntile0 + nt;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kZStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 4) {
+    if (lane == 0) {
+      const uint64_t pol_w = l2_policy(true);
+      const double* wt = p.W + (long long)ntile * nkc * (kZBBytes / 8);
+      const double* at = p.A + (long long)mt * nkc * (kZABytes / 8);
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int s = kc % kZStages;
+        if (kc >= kZStages) mbar_wait(&empty[s], ((kc / kZStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kZABytes + kZBBytes);
+        bulk_load_h(sA + s * (kZABytes / 8), at + (long long)kc * (kZABytes / 8), kZABytes, &full[s], pol_w);
+        bulk_load_h(sB + s * (kZBBytes / 8), wt + (long long)kc * (kZBBytes / 8), kZBBytes, &full[s], pol_w);
+      }
+    }
+    return;
+  }
+  const int wm = warp >> 1, wn = warp & 1;
+  const int rq = lane & 3, cq = lane >> 2;
+  const uint64_t pol_c = l2_policy(false);
+  double acc1[2][4][2], acc2[2][4][2], acc3[2][4][2];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni) {
+    const int c = ntile * kZBN + wn * 16 + ni * 8 + cq;
+    const bool cv = c >= p.c_begin && c < p.n_sel;
+    int sy = 0;
+    ld1p_i(sy, p.sy + (cv ? c : 0), cv);
+    const double* xc = reinterpret_cast<const double*>(p.X + (long long)(cv ? c : 0) * p.ldx);
+    double v[4][4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i0 = m0 + wm * 32 + mi * 8 + 2 * rq;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[mi][q] = 0.0;
+      ld2h(v[mi][0], v[mi][1], xc + 2 * i0, cv && i0 < p.rows && i0 >= p.row_lo, pol_c);
+      ld2h(v[mi][2], v[mi][3], xc + 2 * i0 + 2, cv && i0 + 1 < p.rows && i0 + 1 >= p.row_lo, pol_c);
+    }
+    if (sy != 0) {   // rare: a scaling decision of Algorithm 3 (exact powers of two)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[mi][q] = ldexp(v[mi][q], sy);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc1[ni][mi][h] = v[mi][2 * h];
+        acc2[ni][mi][h] = 0.0;
+        acc3[ni][mi][h] = __dadd_rn(v[mi][2 * h + 1], v[mi][2 * h]);
+      }
+    }
+  }
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int s = kc % kZStages;
+    mbar_wait(&full[s], (kc / kZStages) & 1);
+    // release the previous stage only now (see k_update_t)
+    if (lane == 0 && kc >= 1 && kc - 1 + kZStages < nkc) mbar_arrive(&empty[(kc - 1) % kZStages]);
+    const double* a = sA + s * (kZABytes / 8);
+    const double* b = sB + s * (kZBBytes / 8);
+#pragma unroll
+    for (int ks = 0; ks < kZBK / 4; ++ks) {
+      double wr[2], wi[2], ws[2], fr[4], fi[4], fs[4];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) {
+        const int o = (ks * kZBN + wn * 16 + ni * 8 + cq) * 4 + rq;
+        wr[ni] = b[o];
+        wi[ni] = b[256 + o];
+        ws[ni] = b[512 + o];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int g = wm * 4 + mi;
+        fr[mi] = a[((g * 3 + 0) * 2 + ks) * 32 + lane];
+        fi[mi] = a[((g * 3 + 1) * 2 + ks) * 32 + lane];
+        fs[mi] = a[((g * 3 + 2) * 2 + ks) * 32 + lane];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          dmma(acc1[ni][mi][0], acc1[ni][mi][1], wr[ni], fr[mi]);
+          dmma(acc2[ni][mi][0], acc2[ni][mi][1], wi[ni], fi[mi]);
+          dmma(acc3[ni][mi][0], acc3[ni][mi][1], ws[ni], fs[mi]);
+        }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni) {
+    const int c = ntile * kZBN + wn * 16 + ni * 8 + cq;
+    const bool cv = c >= p.c_begin && c < p.n_sel;
+    double* xc = reinterpret_cast<double*>(p.X + (long long)(cv ? c : 0) * p.ldx);
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i0 = m0 + wm * 32 + mi * 8 + 2 * rq;
+      double o[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        o[h][0] = __dsub_rn(acc1[ni][mi][h], acc2[ni][mi][h]);
+        o[h][1] = __dsub_rn(__dsub_rn(acc3[ni][mi][h], acc1[ni][mi][h]), acc2[ni][mi][h]);
+      }
+      st2h(xc + 2 * i0, o[0][0], o[0][1], cv && i0 < p.rows && i0 >= p.row_lo, pol_c);
+      st2h(xc + 2 * i0 + 2, o[1][0], o[1][1], cv && i0 + 1 < p.rows && i0 + 1 >= p.row_lo, pol_c);
+    }
+  }
 }
 
 // (4) consistency and normalisation: e_c = min_I e_seg[I][c]; X <- ldexp(X, e_c - e_seg) / xmax
@@ -399,10 +594,9 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   if (m > 0 && !X_) return -7;
   if (ldx < std::max(1, m)) return -8;
   cudaStream_t st;
-  cublasHandle_t blas;
-  int mb_ctx;
+  int mb_ctx, la_mode;
   zz_info_t* info;
-  int r = ctx_acquire(&st, &blas, &mb_ctx, &info);
+  int r = ctx_acquire(&st, &mb_ctx, &la_mode, &info);
   if (r) return r;
   memset(info, 0, sizeof(*info));
   info->m = m;
@@ -422,11 +616,15 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   double2* X = reinterpret_cast<double2*>(X_);
   if (n == 0) return 0;
   // workspace (stream-ordered)
+  const int nkS_max = (nb + kZBK - 1) / kZBK;
+  const int n_nt = (n + kZBN - 1) / kZBN;
+  const size_t wsz = (size_t)n_nt * 2 * nkS_max * (kZBBytes / 8);   // doubles per W set
+  const size_t apk = (size_t)((m + kZBM - 1) / kZBM) * 2 * nkS_max * (kZABytes / 8);   // packed panel
   size_t off[13], tot = 0;
   const size_t sz[13] = {sizeof(int) * n, sizeof(double2) * n, sizeof(double) * n, sizeof(int) * n, sizeof(double) * n,
                          sizeof(int) * (size_t)M * n, sizeof(double) * (size_t)M * n, sizeof(double) * m,
-                         sizeof(double) * m, sizeof(double2) * 4 * (size_t)nb * n,
-                         sizeof(double2) * 2 * (size_t)nb * (size_t)m, sizeof(int) * 4, sizeof(int) * n};
+                         sizeof(double) * m, sizeof(double) * 2 * wsz, sizeof(int) * 4, sizeof(int) * 2 * n,
+                         sizeof(double) * apk};
   for (int i = 0; i < 13; ++i) { off[i] = tot; tot += align256(sz[i]); }
   ZWork wk;
   ZCK(wk.alloc(tot, st));
@@ -440,10 +638,10 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   double* d_nrmh = reinterpret_cast<double*>(base + off[6]);
   double* d_cmS = reinterpret_cast<double*>(base + off[7]);
   double* d_cmT = reinterpret_cast<double*>(base + off[8]);
-  double2* d_B = reinterpret_cast<double2*>(base + off[9]);
-  double2* d_A = reinterpret_cast<double2*>(base + off[10]);
-  int* d_status = reinterpret_cast<int*>(base + off[11]);
-  int* d_sy = reinterpret_cast<int*>(base + off[12]);
+  double* d_W = reinterpret_cast<double*>(base + off[9]);
+  int* d_status = reinterpret_cast<int*>(base + off[10]);
+  int* d_sy = reinterpret_cast<int*>(base + off[11]);
+  double* d_A = reinterpret_cast<double*>(base + off[12]);
   int launches = 0;
   ZCK(cudaMemcpyAsync(d_jcol, jcol.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
   const int big = 0x7fffffff;
@@ -460,6 +658,8 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   if (hstatus != big) return (hstatus & 1) == kZErrCplxDiag ? ZZ_ERR_CPLXDIAG : ZZ_ERR_NONFINITE;
   const size_t smem = sizeof(double2) * 2 * nb * nb + sizeof(double) * 2 * kZMaxNB;
   ZCK(cudaFuncSetAttribute(k_zdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ZCK(cudaFuncSetAttribute(k_zupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, kZUSmem));
+  ZCK(cudaFuncSetAttribute(k_zupdate, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int nsm = 148;
   {
     int dev;
@@ -481,15 +681,21 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   // Lookahead (DESIGN.md s.6 "Complex pencils"): the update of step I is split into the band
   // (the rows of tile I-1) and the rest; the solve of tile I-1 runs on a high-priority stream
   // beside the rest.  The scaling decisions use the pending bound (R21), so the solve needs
-  // nothing from the rest; sigma_Y is applied by k_zscale_pending on the update stream.
-  const char* la_env = getenv("ZZ_ZLOOKAHEAD");
-  const bool la = (la_env ? atoi(la_env) != 0 : true) && Itop >= 1;
+  // nothing from the rest; W and sy alternate between two sets by step parity, so the solve of
+  // tile I-1 never overwrites what the rest of step I's update still reads.
+  const bool la = la_mode != 0 && Itop >= 1;   // zz_set_lookahead(0) turns it off
   cudaStream_t hp = nullptr;
   cudaEvent_t ev_band = nullptr, ev_diag = nullptr;
   struct Guard {
-    cudaStream_t& h; cudaEvent_t& a; cudaEvent_t& b;
-    ~Guard() { if (h) cudaStreamDestroy(h); if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
-  } guard{hp, ev_band, ev_diag};
+    cudaStream_t& h; cudaEvent_t& a; cudaEvent_t& b; cudaStream_t st;
+    ~Guard() {
+      // on every exit (errors included) the work queued on the high-priority stream has
+      // finished before the workspace is released on st (ZWork, stream-ordered)
+      if (h) { cudaStreamSynchronize(h); cudaStreamDestroy(h); }
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } guard{hp, ev_band, ev_diag, st};
   if (la) {
     int lo, hi;
     ZCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -497,11 +703,6 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     ZCK(cudaEventCreateWithFlags(&ev_band, cudaEventDisableTiming));
     ZCK(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
   }
-  // Gauss's three-multiplication complex product (cublasZgemm3m, default; ZZ_Z3M=0 selects
-  // ZGEMM): 25 % fewer real flops; its (Ar + Ai)(Br + Bi) partial sums are up to twice the
-  // four-multiplication bound, so Algorithm 3's tau doubles (R23)
-  const bool use3m = !(getenv("ZZ_Z3M") && atoi(getenv("ZZ_Z3M")) == 0);
-  const size_t bsz = 2 * (size_t)nb * n;
   auto diag = [&](int I, cudaStream_t s) -> cudaError_t {
     const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
     ZDiagParams p;
@@ -511,46 +712,62 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.e_pend = d_epend; p.nYb = d_nYb;
     p.e_seg = d_eseg + (size_t)I * n;
     p.nrmh_seg = d_nrmh + (size_t)I * n;
-    p.B = d_B + (size_t)(I & 1) * bsz;
-    p.sy = d_sy;
-    p.tau_mul = use3m ? 4.0 : 2.0;
+    p.W = d_W + (size_t)(I & 1) * wsz;
+    p.nkS = (nt + kZBK - 1) / kZBK;
+    p.sy = d_sy + (size_t)(I & 1) * n;
     const int grid = std::min((n_act + kZWarps - 1) / kZWarps, nsm);   // one 132 KB CTA per SM
     k_zdiag<<<grid, kZWarps * 32, smem, s>>>(p);
     ++launches;
     return cudaGetLastError();
   };
-  const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
-  // Y(row0:row0+rows, cs:n) <- Y - [S_panel | T_panel](row0:row0+rows, :) [sigma beta X_I ; -sigma alpha X_I]
-  auto gemm = [&](int I, int row0, int rows) -> int {
-    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
-    if ((use3m ? cublasZgemm3m : cublasZgemm)(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, n_act, 2 * nt, &mone,
-                    reinterpret_cast<const cuDoubleComplex*>(d_A + row0), r0,
-                    reinterpret_cast<const cuDoubleComplex*>(d_B + (size_t)(I & 1) * bsz), 2 * nt, &one,
-                    reinterpret_cast<cuDoubleComplex*>(X + (size_t)cs * ldx + row0), ldx) != CUBLAS_STATUS_SUCCESS)
-      return ZZ_ERR_CUDA;
+  // the panel of step I in fragment order (rows 0 .. r0 - 1)
+  auto pack = [&](int I) -> cudaError_t {
+    const int r0 = I * nb, nt = std::min(nb, m - r0), nkS = (nt + kZBK - 1) / kZBK;
+    k_zpack<<<dim3((r0 + kZBM - 1) / kZBM, 2 * nkS), 256, 0, st>>>(S, lds, T, ldt, r0, nt, nkS, d_A);
+    ++launches;
+    return cudaGetLastError();
+  };
+  // Y(row0:row0+rows, cs:n) <- 2^sy Y + [S_panel | T_panel](row0:row0+rows, :) W_I
+  auto update = [&](int I, int row0, int rows) -> cudaError_t {
+    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I];
+    ZUpdParams up;
+    up.row_lo = row0;
+    up.rows = row0 + rows;
+    up.nkc = 2 * ((nt + kZBK - 1) / kZBK);
+    up.c_begin = cs;
+    up.n_sel = n;
+    up.ntile0 = cs / kZBN;
+    up.mtile0 = row0 / kZBM;
+    up.X = X;
+    up.ldx = ldx;
+    up.A = d_A;
+    up.W = d_W + (size_t)(I & 1) * wsz;
+    up.sy = d_sy + (size_t)(I & 1) * n;
+    const int n_mt = (row0 + rows - 1) / kZBM - up.mtile0 + 1, n_ntl = n_nt - up.ntile0;
+    if (rows <= 0 || n_ntl <= 0) return cudaSuccess;
+    // one tile per CTA: CTAs retire after each tile, so the high-priority diagonal solve of the
+    // lookahead finds free SMs (measured: a persistent grid of 2 CTAs per SM was slower with it)
+    k_zupdate<<<n_mt * n_ntl, kZUThreads, kZUSmem, st>>>(up, n_mt, n_ntl);
     ++launches;
     info->update_launches++;
-    return 0;
+    return cudaGetLastError();
   };
   if (Itop >= 0) ZCK(diag(Itop, st));
   for (int I = Itop; I >= 0; --I) {
-    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
+    const int r0 = I * nb;
     if (la && I < Itop) ZCK(cudaStreamWaitEvent(st, ev_diag, 0));
     if (r0 == 0) break;
-    k_zscale_pending<<<(n_act + 7) / 8, 256, 0, st>>>(X, ldx, r0, cs, n_act, d_sy);
-    k_zpanel<<<dim3((r0 + 255) / 256 > 64 ? 64 : (r0 + 255) / 256, 2 * nt), 256, 0, st>>>(S, lds, T, ldt, r0, nt, d_A);
-    launches += 2;
-    ZCK(cudaGetLastError());
+    ZCK(pack(I));
     if (la) {
       const int rb = r0 - nb;   // tile I-1 is a full tile
-      if ((r = gemm(I, rb, nb))) return r;
+      ZCK(update(I, rb, nb));
       ZCK(cudaEventRecord(ev_band, st));
       ZCK(cudaStreamWaitEvent(hp, ev_band, 0));
       ZCK(diag(I - 1, hp));
       ZCK(cudaEventRecord(ev_diag, hp));
-      if (rb > 0 && (r = gemm(I, 0, rb))) return r;
+      if (rb > 0) ZCK(update(I, 0, rb));
     } else {
-      if ((r = gemm(I, 0, r0))) return r;
+      ZCK(update(I, 0, r0));
       ZCK(diag(I - 1, st));
     }
   }

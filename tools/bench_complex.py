@@ -25,6 +25,7 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--no-check", action="store_true")
+ap.add_argument("--lookahead", type=int, default=1)
 args = ap.parse_args()
 
 m = args.m
@@ -33,6 +34,7 @@ S, T = gen.complex_pencil(m, seed=args.seed)
 tgen = time.time() - t0
 zz.init(0)
 zz.set_tile(args.tile)
+zz.set_lookahead(args.lookahead)
 Sd = torch.from_numpy(S).cuda().t().contiguous().t()
 Td = torch.from_numpy(T).cuda().t().contiguous().t()
 st = torch.cuda.current_stream()
@@ -54,7 +56,7 @@ info = zz.last_info()
 out = {"metric": "seconds & FP64 TFLOP/s, all eigenvectors of a complex Schur pencil (zz_ztgevc)",
        "m": m, "tile": info["mb"], "steps": args.steps, "warmup": args.warmup,
        "seconds_per_call": sec, "flops_nominal": F, "value": F / sec * 1e-12, "unit": "TFLOP/s",
-       "update_product": "zgemm" if os.environ.get("ZZ_Z3M", "1") == "0" else "gauss3m",
+       "update_product": "gauss3m (k_zupdate, three DMMA contractions)", "lookahead": args.lookahead,
        # with Gauss 3M the executed real flops of the update are 25 % fewer than F_z: the
        # ratio below is then an effective (time-to-solution) figure, not a pipe fraction
        "fraction_of_fp64_peak": F / sec * 1e-12 / 37.0,
