@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--left", action="store_true", help="also time zz_tgevc_left (left eigenvectors)")
     ap.add_argument("--back", action="store_true",
                     help="also time zz_tgevc_back (back-transformation W = V X, xTGEVC HOWMNY='B')")
+    ap.add_argument("--subsets", default="",
+                    help="comma-separated fractions of randomly selected eigenvalues to time (select, PAPER.md:268)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -449,6 +451,35 @@ def main():
                        "seconds_per_step": tl, "value": F / tl * 1e-12, "unit": "TFLOP/s"}
         Yd = None
         torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and args.subsets:
+        # subsets E of the eigenvalues: uniformly random selections; the work is
+        # F(select) = sum over the selected columns of 2 r_c (r_c - 1); reported against the
+        # time the full solve's rate would give for that work
+        out = []
+        rate = F / t
+        for fr in [float(x) for x in args.subsets.split(",") if x]:
+            sel = (np.random.default_rng(args.seed + 11).random(m) < fr).astype(np.int32)
+            Fs = nominal_flops(blocks, sel)
+            n_s = sum(sz for j, sz in blocks if sel[j] or (sz == 2 and sel[j + 1]))
+            Xs = zz.empty_colmajor(m, max(n_s, 1), device=dev)[:, :n_s]
+            Es = torch.empty(max(n_s, 1), dtype=torch.int32, device=dev)[:n_s]
+            for _ in range(2):
+                zz.tgevc(Sd, Td, select=sel, X=Xs, col_scale_exp=Es, n_sel=n_s)
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            ks = max(1, args.steps)
+            s0.record(st)
+            for _ in range(ks):
+                zz.tgevc(Sd, Td, select=sel, X=Xs, col_scale_exp=Es, n_sel=n_s)
+            s1.record(st)
+            torch.cuda.synchronize()
+            ts_ = s0.elapsed_time(s1) / 1e3 / ks
+            out.append({"fraction": fr, "columns": int(n_s), "flops": Fs, "seconds": ts_,
+                        "tflops": Fs / ts_ * 1e-12, "seconds_at_full_rate": Fs / rate,
+                        "ratio_to_full_rate_time": ts_ / (Fs / rate)})
+            Xs = Es = None
+        res["subsets"] = out
     if rank == 0 and world == 1 and args.back:
         # back-transformation leg (a separate capability, not part of the headline metric):
         # V is a seeded Gaussian N(0, 1/m) made on the device -- the work does not depend on
