@@ -1,0 +1,32 @@
+#!/bin/bash
+# round evidence: smoke, full GPU tests, default bench, subsets, ncu launch list + full captures,
+# per-config sweep, sanitizers
+TAG=${1:-r02p}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/${TAG}_gpu.txt 2>&1
+python -c "from paper_2003_04776_b200 import _build; _build.build()"
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/${TAG}_smoke.log 2>&1; echo "smoke exit $?"; tail -2 $OUT/${TAG}_smoke.log
+if [ "${TESTS:-1}" = "1" ]; then
+timeout 2000 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/${TAG}_pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -2 $OUT/${TAG}_pytest_gpu.log
+fi
+timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "bench exit $?"
+python -c "import json; d=json.loads(open('$OUT/${TAG}_bench.json').read()); print('C4', d['ms_per_step'], d['value'], d['roofline']['frac'], d['e2e']['value'])"
+timeout 900 python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-roofline --subsets 0.01,0.1 > $OUT/${TAG}_subsets.json 2> $OUT/${TAG}_subsets.err; echo "subsets exit $?"
+python -c "import json; d=json.loads(open('$OUT/${TAG}_subsets.json').read()); print(d['subsets'])"
+if [ "${SWEEP:-1}" = "1" ]; then
+timeout 900 python tools/sweep.py > $OUT/${TAG}_sweep.json 2> $OUT/${TAG}_sweep.err; echo "sweep exit $?"
+fi
+if [ "${NCU:-1}" = "1" ]; then
+  CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-roofline"
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/${TAG}_launches.csv $CMD > $OUT/${TAG}_ncu_launches.log 2>&1; echo "ncu launches exit $?"
+  CMD2="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-roofline"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+      -k regex:k_update_tILi1E -s 30 -c 1 -o $OUT/${TAG}_update $CMD2 > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu update exit $?"
+fi
+if [ "${SAN:-1}" = "1" ]; then
+  for tool in memcheck racecheck synccheck; do
+    timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > $OUT/${TAG}_san_$tool.log 2>&1; echo "sanitizer $tool exit $?"; tail -3 $OUT/${TAG}_san_$tool.log
+  done
+fi
