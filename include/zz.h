@@ -202,10 +202,12 @@ int zz_tgevc_host(int m, const double* S, int lds, const double* T, int ldt, con
  *                  W must not overlap V, S or T.                              [args 9,10]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: as zz_tgevc (the exponents of the
  *                  (S,T) eigenvectors before their normalisation)             [arg 11]
- * The product runs as column blocks of 256 columns with K = 1 + the block's largest r_c
- * (cuBLAS DGEMM: X is block-upper-triangular, so the work is ~ m^3 flop for all
- * eigenvectors instead of 2 m^3); normalisation is one pass over W.  The library keeps an
- * m x n_sel workspace for X.  Status codes as zz_tgevc; -100 also covers a cuBLAS error.
+ * The product is one FP64 tensor-core contraction (DMMA) of this library over tiles of 64
+ * columns with K = 1 + the tile's largest r_c (X is block-upper-triangular, so the work is
+ * ~ m^3 flop for all eigenvectors instead of 2 m^3); the column maxima come from its epilogue
+ * and the normalisation is one pass over W.  The library keeps an m x n_sel workspace for X
+ * and a tile-packed copy of its upper part.  V may have any leading dimension (an odd one
+ * or a misaligned base is copied to an aligned workspace).  Status codes as zz_tgevc.
  */
 int zz_tgevc_back(int m, const double* S, int lds, const double* T, int ldt, const int* select,
                   const double* V, int ldv, double* W, int ldw, int* col_scale_exp);
@@ -233,20 +235,23 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
  * with complex entries (readings R18-R21).
  *   m              order (m >= 0)                                                [arg 1]
  *   S, lds         DEVICE, m x m complex column-major, INTERLEAVED (re, im) doubles
- *                  (LAPACK COMPLEX*16 layout); lds in complex elements; never written.
- *                  The strictly lower part is never read.                      [args 2,3]
- *   T, ldt         DEVICE, as S; Im T_jj must be 0 (else -107)                  [args 4,5]
+ *                  (LAPACK COMPLEX*16 layout), base 16-byte aligned (else -2); lds in
+ *                  complex elements; never written.  The strictly lower part is never
+ *                  read.                                                        [args 2,3]
+ *   T, ldt         DEVICE, as S (16-byte aligned, else -4); Im T_jj must be 0 (else -107)
+ *                                                                                [args 4,5]
  *   select         HOST int[m] or NULL (all); select[j] != 0 picks eigenvalue j; output
  *                  columns in increasing j.                                      [arg 6]
- *   X, ldx         DEVICE, m x n_sel complex interleaved, ldx (complex elements) >= m;
- *                  written completely: z_i = 0 for i > j, normalised as ZTGEVC does,
+ *   X, ldx         DEVICE, m x n_sel complex interleaved, ldx (complex elements) >= m,
+ *                  base 16-byte aligned (else -7); written completely: z_i = 0 for i > j, normalised as ZTGEVC does,
  *                  max_i (|Re z_i| + |Im z_i|) = 1, from a real positive z_j before
  *                  normalisation; alpha = beta = 0 gives e_j.                  [args 7,8]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: exponents as zz_tgevc.            [arg 9]
- * Tiles of zz_set_tile() rows when it is 32, 48 or 64, else 64 (fastest, profiles/r01o_complex_tile_sweep.txt).  The update of each step is one complex
- * contraction of K = 2 x tile over a copy of the S and T panels (cuBLAS ZGEMM3M, Gauss's
- * three-multiplication form, by default; ZGEMM with the environment ZZ_Z3M=0); the solves,
- * scaling decisions, panel copies and normalisation are this library's kernels.  The call
+ * Tiles of zz_set_tile() rows when it is 32, 48 or 64, else 64 (fastest,
+ * profiles/r01o_complex_tile_sweep.txt).  The update of each step is one complex contraction
+ * of K = 2 x tile (this library's DMMA kernel, Gauss's three-multiplication form, DESIGN.md
+ * R23) over a fragment-ordered copy of the S and T panels; zz_set_lookahead(0) runs the
+ * diagonal solves in line instead of on a high-priority stream.  The call
  * allocates its workspace stream-ordered (cudaMallocAsync) and returns after the stream has
  * completed.  Status codes as zz_tgevc (-104 non-finite diagonal entry, -107). */
 int zz_ztgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,

@@ -14,6 +14,7 @@
 // Readings R18-R21 of DESIGN.md; the pending-row maximum is carried as an upper bound
 // (R21) instead of being measured, so the update needs no epilogue.
 #include <cuda.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -593,6 +594,12 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   if (ldt < std::max(1, m)) return -5;
   if (m > 0 && !X_) return -7;
   if (ldx < std::max(1, m)) return -8;
+  // COMPLEX*16 is read and written as 16-byte (re, im) pairs: the bases must be 16-byte
+  // aligned (a misaligned access would be a sticky fault of the CUDA context)
+  auto misaligned = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) != 0; };
+  if (m > 0 && misaligned(S_)) return -2;
+  if (m > 0 && misaligned(T_)) return -4;
+  if (m > 0 && misaligned(X_)) return -7;
   cudaStream_t st;
   int mb_ctx, la_mode;
   zz_info_t* info;

@@ -18,7 +18,10 @@ for r in rows[hi + 1:]:
     n = next((k for k in KEYS if k in r[ki]), "library GEMM (cuBLAS/CUTLASS)" if ("gemm" in r[ki].lower() or "cutlass" in r[ki].lower()) else r[ki][:40])
     d[n][0] += 1
     d[n][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
-calls = d[sys.argv[2]][0] if len(sys.argv) > 2 and d[sys.argv[2]][0] else 1
+calls = 1
+if len(sys.argv) > 2:
+    mk = [v[0] for k, v in d.items() if k.startswith(sys.argv[2])]
+    calls = max(mk) if mk and max(mk) else 1
 tot = sum(v[1] for v in d.values())
 print("# %s: per-call device time (ncu, cold-cache, serialised; %d calls in the list)" % (sys.argv[1], calls))
 print("%-32s %9s %12s %8s" % ("kernel", "launches", "ms/call", "share"))
