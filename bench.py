@@ -228,7 +228,7 @@ def main():
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-blocks", type=int, default=192)
-    ap.add_argument("--ref-blocks", type=int, default=24)
+    ap.add_argument("--ref-blocks", type=int, default=192)
     ap.add_argument("--left", action="store_true", help="also time zz_tgevc_left (left eigenvectors)")
     ap.add_argument("--back", action="store_true",
                     help="also time zz_tgevc_back (back-transformation W = V X, xTGEVC HOWMNY='B')")

@@ -35,3 +35,24 @@ def test_nominal_flops_closed_form():
     # the update kernels' algorithmic work is F minus the in-tile (diagonal solve) part
     f_upd, per, M = bench.update_flops(blocks, m, 128)
     assert M == 8 and len(per) == M - 1 and 0 < f_upd < bench.nominal_flops(blocks)
+
+
+def test_gpus_n_outside_torchrun_starts_ranks(monkeypatch):
+    """--gpus N > 1 without torchrun's environment re-launches bench.py through torchrun with
+    N ranks (one per GPU) and the same flags (the driver's `bench.py --gpus 8`)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    try:
+        bench.main()
+    except SystemExit as e:
+        assert e.code == 0
+    assert len(calls) == 1
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4"
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"] and cmd[-5].endswith("bench.py")
