@@ -7,10 +7,13 @@
 //
 // NCCL is opened with dlopen("libnccl.so.2") when a communicator is first requested, so the
 // library itself loads without it (a process that imported torch gets torch's NCCL: the
-// dynamic loader matches the soname of the already-loaded copy).
+// dynamic loader matches the soname of the already-loaded copy).  The environment variable
+// ZZ_NCCL_LIB may name another library with the same entry points (the tests' in-process
+// multi-rank transport, tests/mock_nccl).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "zz_internal.cuh"
 
@@ -23,10 +26,12 @@ int g_api_state = 0;   // 0 untried, 1 loaded, -1 unavailable
 
 const NcclApi* nccl_api() {
   if (g_api_state == 0) {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    // ZZ_NCCL_LIB: another library with NCCL's entry points (tests/mock_nccl: an in-process
+    // transport that lets several ranks share one GPU in the tests; read once, at first use)
+    const char* names[] = {getenv("ZZ_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
     void* h = nullptr;
     for (const char* n : names)
-      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+      if (n && (h = dlopen(n, RTLD_NOW | RTLD_LOCAL))) break;
     g_api_state = -1;
     if (h) {
       g_api.getUniqueId = reinterpret_cast<decltype(g_api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
