@@ -633,6 +633,11 @@ def test_lookahead_forced_on_stress_recomputes(zz):
         X1, e1, info = solve(zz, S, T, mb=64)
         assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
         assert info["lookahead_redo"] == 1
+        # the same with an odd ldx (X solved in the library's aligned workspace): the
+        # recomputation must land in the caller's X, not in the workspace
+        X2, e2, info3 = solve(zz, S, T, mb=64, ldx=2001)
+        assert info3["lookahead_redo"] == 1
+        assert np.array_equal(X0, X2) and np.array_equal(e0, e2)
         # a small well-scaled pencil forced on: no redo, bitwise
         S2, T2, _ = gen.config("C2", seed=1)
         zz.set_lookahead(0)
