@@ -126,6 +126,13 @@ int zz_set_stream(void* stream);
  * row (reading R12).  Returns 0, -103 or -106. */
 int zz_set_tile(int mb);
 
+/* CUDA graph of the wavefront: 1 (default) captures the launch sequence
+ * of a call's wavefront once and replays it while the plan (sizes, block structure,
+ * selection, tile, step groups, lookahead) and every pointer it uses are unchanged -- the
+ * same kernels in the same order, so results are bitwise those of 0 (plain stream launches).
+ * Not used by the host-staged or collective paths.  Returns 0 or -103. */
+int zz_set_graphs(int on);
+
 /* Per-kernel timing of the robust update with CUDA events (0 off, 1 on): fills
  * zz_info_t.ms_update.  Adds an event pair per step; used by bench.py for the roofline. */
 int zz_set_timing(int on);

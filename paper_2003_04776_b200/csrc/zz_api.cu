@@ -59,6 +59,12 @@ struct Context {
   int timing = 0;
   // step groups of the wavefront: k consecutive steps share one update (zz_set_fusion)
   int fusion = 4;
+  // CUDA graph of the wavefront (zz_set_graphs): the last captured plan and its replayable exec
+  int graphs = 1;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap = nullptr;   // capture stream
+  uint64_t gkey = 0;
+  int g_nupd = 0, g_nfused = 0, g_launches = 0;
   // lookahead (zz_set_lookahead): the chain of solves runs on a high-priority stream beside
   // the bulk of the previous group's update (DESIGN.md s.6 "Lookahead"); 1 = automatic
   int lookahead = 1;
@@ -100,6 +106,11 @@ struct Context {
     ev_la.clear();
     if (ev_in) { cudaEventDestroy(ev_in); cudaEventDestroy(ev_out); }
     ev_in = ev_out = nullptr;
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    gkey = 0;
+    if (cap) cudaStreamDestroy(cap);
+    cap = nullptr;
     if (hi) cudaStreamDestroy(hi);
     hi = nullptr;
     Xb.release();
@@ -577,8 +588,6 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     CK(c->sYb.ensure(sizeof(int) * (size_t)n));
     sY_set[1] = c->sYb.as<int>();
     ms = c->hi;
-    CK(cudaEventRecord(c->ev_in, st));
-    CK(cudaStreamWaitEvent(ms, c->ev_in, 0));
   }
   int n_la_ev = 0;
   int gpar = 0;                      // W / sY set of the current group (lookahead)
@@ -681,141 +690,214 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
     up.vec = vec;
     return up;
   };
-  int I = M - 1;
-  while (I >= 0) {
-    int r = panel_ready(I);
-    if (r) return r;
-    if (tile_item[I] >= n_items) { --I; continue; }
-    // Step groups are fixed by the tile index alone (groups of `fusion` consecutive steps
-    // counted from M-1), not by which steps have active columns: a step that opens the
-    // solve in the middle of its group runs the group's remaining steps, so a column's
-    // operations do not depend on the selection (sharding, select).  The last step of a
-    // fused group needs rows above it (index >= 1).
-    int len = 1;
-    if (can_fuse) {
-      len = fusion - (M - 1 - I) % fusion;
-      while (len > 1 && I - (len - 1) < 1) --len;
+  // the wavefront proper: a fixed sequence of launches for a given plan (no host decision
+  // depends on device data inside it), captured once into a CUDA graph and replayed while
+  // the plan and every pointer it uses stay the same
+  auto wavefront = [&]() -> int {
+    if (la) {   // fork the chain's stream from the caller's (inside a capture: joins the graph)
+      CK(cudaEventRecord(c->ev_in, st));
+      CK(cudaStreamWaitEvent(ms, c->ev_in, 0));
     }
-    auto nks_of = [&](int t) { return ceil_div(ts[t + 1] - ts[t], kBK); };
-    if (len >= 2) {
-      // ---- a step group (I, I-1, ..., L = I-len+1): diag of each step, thin updates of the
-      // group's own band (the rows of its later tiles) after every step but the last, and one
-      // update of all rows above tile L with K = [tile L | ... | tile I] ----
-      const int L = I - len + 1;
-      double* Wg[kMaxGroup];
-      Wg[0] = P.W;
-      for (int k = 1; k < len; ++k) Wg[k] = c->Wx[k - 1].as<double>();
-      if (la && gpar == 1)
-        for (int k = 0; k < len; ++k) Wg[k] = c->Wy[k].as<double>();
-      for (int sgi = 0; sgi < len; ++sgi) {
-        const int X = I - sgi;
-        if (sgi > 0 && (r = panel_ready(X))) return r;
-        Diag2Params o;
-        memset(&o, 0, sizeof(o));
-        if (sgi == 0) {
-          o.fused = 0;
-          o.grp_slot = 0;
-          o.n_band_reset = len - 2;
-          o.use_bound = la && prev_bound;
-          if (la && !prev_bound && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
-        } else if (sgi < len - 1) {
-          o.fused = 2;
-          o.grp_slot = sgi;
-          o.band_in = 2 + (sgi - 1);
-        } else {
-          o.fused = 3;
-          o.grp_slot = -1;
-          o.n_prev = len - 1;
-          for (int k = 0; k < len - 1; ++k) {
-            o.prev_I[k] = I - k;
-            o.prev_cs[k] = cs[I - k];
-            o.prev_nks[k] = nks_of(I - k);
-            o.prev_W[k] = Wg[k];
-          }
-          o.zero_pend_end = cs[I + 1];       // tips of the group start from zero pending rows
-          o.record_bound = la;
-          // the decision needs the pending maximum of the rows above tile L (the bulk update
-          // of the previous group)
-          if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
-        }
-        if ((r = diag(X, Wg[sgi], &o))) return r;
-        if (sgi < len - 1) {
-          UpdParams th = base_up(X);         // rows of the group's tiles below X with W_X
-          th.row_lo = ts[L];
-          th.W = Wg[sgi];
-          if (sgi + 1 < len - 1) {           // band maximum for the next (middle) step
-            th.max_row = ts[X - 1];
-            th.nY_out = P.nY + (size_t)(2 + sgi) * n;
+    int I = M - 1;
+    while (I >= 0) {
+      int r = panel_ready(I);
+      if (r) return r;
+      if (tile_item[I] >= n_items) { --I; continue; }
+      // Step groups are fixed by the tile index alone (groups of `fusion` consecutive steps
+      // counted from M-1), not by which steps have active columns: a step that opens the
+      // solve in the middle of its group runs the group's remaining steps, so a column's
+      // operations do not depend on the selection (sharding, select).  The last step of a
+      // fused group needs rows above it (index >= 1).
+      int len = 1;
+      if (can_fuse) {
+        len = fusion - (M - 1 - I) % fusion;
+        while (len > 1 && I - (len - 1) < 1) --len;
+      }
+      auto nks_of = [&](int t) { return ceil_div(ts[t + 1] - ts[t], kBK); };
+      if (len >= 2) {
+        // ---- a step group (I, I-1, ..., L = I-len+1): diag of each step, thin updates of the
+        // group's own band (the rows of its later tiles) after every step but the last, and one
+        // update of all rows above tile L with K = [tile L | ... | tile I] ----
+        const int L = I - len + 1;
+        double* Wg[kMaxGroup];
+        Wg[0] = P.W;
+        for (int k = 1; k < len; ++k) Wg[k] = c->Wx[k - 1].as<double>();
+        if (la && gpar == 1)
+          for (int k = 0; k < len; ++k) Wg[k] = c->Wy[k].as<double>();
+        for (int sgi = 0; sgi < len; ++sgi) {
+          const int X = I - sgi;
+          if (sgi > 0 && (r = panel_ready(X))) return r;
+          Diag2Params o;
+          memset(&o, 0, sizeof(o));
+          if (sgi == 0) {
+            o.fused = 0;
+            o.grp_slot = 0;
+            o.n_band_reset = len - 2;
+            o.use_bound = la && prev_bound;
+            if (la && !prev_bound && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+          } else if (sgi < len - 1) {
+            o.fused = 2;
+            o.grp_slot = sgi;
+            o.band_in = 2 + (sgi - 1);
           } else {
-            th.max_row = 0;
+            o.fused = 3;
+            o.grp_slot = -1;
+            o.n_prev = len - 1;
+            for (int k = 0; k < len - 1; ++k) {
+              o.prev_I[k] = I - k;
+              o.prev_cs[k] = cs[I - k];
+              o.prev_nks[k] = nks_of(I - k);
+              o.prev_W[k] = Wg[k];
+            }
+            o.zero_pend_end = cs[I + 1];       // tips of the group start from zero pending rows
+            o.record_bound = la;
+            // the decision needs the pending maximum of the rows above tile L (the bulk update
+            // of the previous group)
+            if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
           }
-          if ((r = update(th, ceil_div(ts[X] - (ts[L] & ~1), kBM), ms))) return r;
+          if ((r = diag(X, Wg[sgi], &o))) return r;
+          if (sgi < len - 1) {
+            UpdParams th = base_up(X);         // rows of the group's tiles below X with W_X
+            th.row_lo = ts[L];
+            th.W = Wg[sgi];
+            if (sgi + 1 < len - 1) {           // band maximum for the next (middle) step
+              th.max_row = ts[X - 1];
+              th.nY_out = P.nY + (size_t)(2 + sgi) * n;
+            } else {
+              th.max_row = 0;
+            }
+            if ((r = update(th, ceil_div(ts[X] - (ts[L] & ~1), kBM), ms))) return r;
+          }
         }
+        UpdParams fu = base_up(L);
+        fu.W = Wg[len - 1];
+        fu.first_end = cs[I + 1];
+        fu.nxs = len - 1;
+        for (int e = 0; e < len - 1; ++e) {    // tiles L+1, ..., I after tile L
+          const int X = L + 1 + e;
+          fu.xt0[e] = ts[X];
+          fu.xnks[e] = nks_of(X);
+          fu.xW[e] = Wg[I - X];
+        }
+        // the next group's band: its tiles L-1 .. L-len_next (the grouping rule of this loop)
+        int len_next = 0;
+        if (la && L - 1 >= 1) {
+          const int In = L - 1;
+          len_next = fusion - (M - 1 - In) % fusion;
+          while (len_next > 1 && In - (len_next - 1) < 1) --len_next;
+        }
+        if (la && len_next >= 1 && ts[L - len_next] > 0) {
+          const int rb = ts[L - len_next];        // rows [rb, ts[L]): the next group's band
+          UpdParams fb = fu;                    // the band first, on the chain's stream
+          fb.row_lo = rb;
+          // the band part measures rows [rb, ts[L-1]) and the bulk rows [0, rb) into the same
+          // buffer (atomicMax: order-independent), so the next group's last decision reads the
+          // maximum over [0, ts[L-1]) exactly as in the plain schedule (base_up(L).max_row)
+          fb.max_row = ts[L - 1];
+          if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
+          cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
+          CK(cudaEventRecord(ev_dec, ms));
+          CK(cudaStreamWaitEvent(st, ev_dec, 0));
+          UpdParams fr = fu;                    // the bulk on the caller's stream
+          fr.rows = rb;
+          fr.max_row = rb;
+          if ((r = update(fr, ceil_div(rb, kBM), st))) return r;
+          ev_rest = c->ev_la[n_la_ev++];
+          CK(cudaEventRecord(ev_rest, st));
+          prev_bound = true;
+        } else {
+          if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+          if ((r = update(fu, ceil_div(ts[L], kBM), ms))) return r;
+          ev_rest = nullptr;
+          prev_bound = false;
+        }
+        nyb = 1 - nyb;
+        gpar ^= (la ? 1 : 0);
+        ++n_fused;
+        I -= len;
+        continue;
       }
-      UpdParams fu = base_up(L);
-      fu.W = Wg[len - 1];
-      fu.first_end = cs[I + 1];
-      fu.nxs = len - 1;
-      for (int e = 0; e < len - 1; ++e) {    // tiles L+1, ..., I after tile L
-        const int X = L + 1 + e;
-        fu.xt0[e] = ts[X];
-        fu.xnks[e] = nks_of(X);
-        fu.xW[e] = Wg[I - X];
-      }
-      // the next group's band: its tiles L-1 .. L-len_next (the grouping rule of this loop)
-      int len_next = 0;
-      if (la && L - 1 >= 1) {
-        const int In = L - 1;
-        len_next = fusion - (M - 1 - In) % fusion;
-        while (len_next > 1 && In - (len_next - 1) < 1) --len_next;
-      }
-      if (la && len_next >= 1 && ts[L - len_next] > 0) {
-        const int rb = ts[L - len_next];        // rows [rb, ts[L]): the next group's band
-        UpdParams fb = fu;                    // the band first, on the chain's stream
-        fb.row_lo = rb;
-        // the band part measures rows [rb, ts[L-1]) and the bulk rows [0, rb) into the same
-        // buffer (atomicMax: order-independent), so the next group's last decision reads the
-        // maximum over [0, ts[L-1]) exactly as in the plain schedule (base_up(L).max_row)
-        fb.max_row = ts[L - 1];
-        if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
-        cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
-        CK(cudaEventRecord(ev_dec, ms));
-        CK(cudaStreamWaitEvent(st, ev_dec, 0));
-        UpdParams fr = fu;                    // the bulk on the caller's stream
-        fr.rows = rb;
-        fr.max_row = rb;
-        if ((r = update(fr, ceil_div(rb, kBM), st))) return r;
-        ev_rest = c->ev_la[n_la_ev++];
-        CK(cudaEventRecord(ev_rest, st));
-        prev_bound = true;
-      } else {
-        if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
-        if ((r = update(fu, ceil_div(ts[L], kBM), ms))) return r;
+      if (la && ev_rest) {               // a single step takes the measured maximum
+        CK(cudaStreamWaitEvent(ms, ev_rest, 0));
         ev_rest = nullptr;
-        prev_bound = false;
       }
-      nyb = 1 - nyb;
-      gpar ^= (la ? 1 : 0);
-      ++n_fused;
-      I -= len;
-      continue;
+      prev_bound = false;
+      if ((r = diag(I, P.W, nullptr))) return r;
+      if (I > 0) {
+        UpdParams up = base_up(I);
+        if ((r = update(up, ceil_div(ts[I], kBM), ms))) return r;
+        nyb = 1 - nyb;
+      }
+      --I;
     }
-    if (la && ev_rest) {               // a single step takes the measured maximum
-      CK(cudaStreamWaitEvent(ms, ev_rest, 0));
-      ev_rest = nullptr;
+    if (la) {                            // join the chain's stream back into the caller's
+      CK(cudaEventRecord(c->ev_out, ms));
+      CK(cudaStreamWaitEvent(st, c->ev_out, 0));
     }
-    prev_bound = false;
-    if ((r = diag(I, P.W, nullptr))) return r;
-    if (I > 0) {
-      UpdParams up = base_up(I);
-      if ((r = update(up, ceil_div(ts[I], kBM), ms))) return r;
-      nyb = 1 - nyb;
+    return 0;
+  };
+  // (not with per-launch timing: the roofline pass measures plain stream launches)
+  const bool use_graph = c->graphs && !hs && n_sel > 0 && !c->timing;
+  if (use_graph) {
+    // the plan's identity: sizes, modes, every pointer the launches use, and the host tables
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](const void* d, size_t bytes) {
+      const unsigned char* q = static_cast<const unsigned char*>(d);
+      for (size_t i = 0; i < bytes; ++i) key = (key ^ q[i]) * 1099511628211ull;
+    };
+    const long long sc[] = {m, mb, n_sel, M, fusion, (long long)la, (long long)c->timing, (long long)vec, ldsu, ldtu,
+                            ldx, nb, n_items};
+    mix(sc, sizeof(sc));
+    const void* ptrs[] = {Su, Tu, X, c->colf.p, c->coli.p, c->items.p, c->tiles.p, c->rows.p, c->blks.p,
+                          c->state.p, c->seg.p, c->norms.p, c->W.p, c->status.p, c->egrp.p, c->nYb.p, c->sYb.p,
+                          c->Wx[0].p, c->Wx[1].p, c->Wx[2].p, c->Wx[3].p, c->Wx[4].p, c->Wy[0].p, c->Wy[1].p,
+                          c->Wy[2].p, c->Wy[3].p, c->Wy[4].p, c->Wy[5].p, c->hi};
+    mix(ptrs, sizeof(ptrs));
+    mix(ts.data(), sizeof(int) * ts.size());
+    mix(col_r.data(), sizeof(int) * col_r.size());
+    mix(item_col.data(), sizeof(int) * item_col.size());
+    mix(real_list.data(), sizeof(int) * real_list.size());
+    mix(pair_list.data(), sizeof(int) * pair_list.size());
+    if (c->gexec && key == c->gkey) {
+      CK(cudaGraphLaunch(c->gexec, st));
+      n_upd = c->g_nupd;
+      n_fused = c->g_nfused;
+      launches += c->g_launches;
+    } else {
+      const int l0 = launches;
+      // captured on a stream of the library's own (the caller's stream may be the legacy
+      // default stream, which cannot be captured); the graph is then launched on st
+      if (!c->cap) CK(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+      const cudaStream_t st0 = st;
+      const bool ms_is_st = ms == st;
+      st = c->cap;
+      if (ms_is_st) ms = c->cap;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      const int r = wavefront();
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(st, &g);
+      st = st0;
+      if (ms_is_st) ms = st0;
+      if (r) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+      }
+      CK(ec);
+      if (c->gexec) cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+      // node priorities as captured: the lookahead's chain keeps its high-priority stream's
+      // priority inside the graph
+      const cudaError_t ei = cudaGraphInstantiateWithFlags(&c->gexec, g, cudaGraphInstantiateFlagUseNodePriority);
+      cudaGraphDestroy(g);
+      CK(ei);
+      c->gkey = key;
+      c->g_nupd = n_upd;
+      c->g_nfused = n_fused;
+      c->g_launches = launches - l0;
+      CK(cudaGraphLaunch(c->gexec, st));
     }
-    --I;
-  }
-  if (la) {                            // join the chain's stream back into the caller's
-    CK(cudaEventRecord(c->ev_out, ms));
-    CK(cudaStreamWaitEvent(st, c->ev_out, 0));
+  } else {
+    if (int r = wavefront()) return r;
   }
   CK(cudaEventRecord(c->e2, st));
   // ---- a7 consistency and normalisation ----
@@ -1290,6 +1372,17 @@ int zz_set_lookahead(int mode) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (mode < 0 || mode > 2) return -1;
   g_ctx->lookahead = mode;
+  return 0;
+}
+
+int zz_set_graphs(int on) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  g_ctx->graphs = on ? 1 : 0;
+  if (!on && g_ctx->gexec) {
+    cudaGraphExecDestroy(g_ctx->gexec);
+    g_ctx->gexec = nullptr;
+    g_ctx->gkey = 0;
+  }
   return 0;
 }
 

@@ -736,3 +736,31 @@ def test_multirank_collective_mock():
                        capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     assert "all ok" in r.stdout
+
+
+def test_graph_replay_bitwise(zz):
+    """CUDA-graph capture / replay of the wavefront (include/zz.h zz_set_graphs): replays,
+    a recapture after new input pointers or a new selection, and the lookahead schedule give
+    the bits of plain stream launches."""
+    cases = [(gen.config("C2", seed=4), 128, None), (gen.config("C3", seed=2, m=4096, n2=614), 128, None),
+             (gen.config("C1", seed=2), 32, None)]
+    try:
+        for (S, T, _), mb, _ in cases:
+            zz.set_graphs(False)
+            X0, e0, _ = solve(zz, S, T, mb=mb)
+            zz.set_graphs(True)
+            Sd, Td = to_dev(S), to_dev(T)
+            for rep in range(3):      # capture, then replays on the same pointers
+                X1, e1, _ = solve(zz, S, T, mb=mb, Sd=Sd, Td=Td)
+                assert np.array_equal(X1, X0) and np.array_equal(e1, e0), rep
+            X2, e2, _ = solve(zz, S, T, mb=mb)   # new input tensors: recaptured
+            assert np.array_equal(X2, X0) and np.array_equal(e2, e0)
+            sel = (np.random.default_rng(1).random(S.shape[0]) < 0.3).astype(np.int32)
+            zz.set_graphs(False)
+            Xs0, es0, _ = solve(zz, S, T, mb=mb, select=sel, Sd=Sd, Td=Td)
+            zz.set_graphs(True)
+            for rep in range(2):
+                Xs1, es1, _ = solve(zz, S, T, mb=mb, select=sel, Sd=Sd, Td=Td)
+                assert np.array_equal(Xs1, Xs0) and np.array_equal(es1, es0)
+    finally:
+        zz.set_graphs(True)
