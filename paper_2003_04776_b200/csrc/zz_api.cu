@@ -10,6 +10,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -151,6 +152,13 @@ thread_local Context* g_ctx = nullptr;
     }                                                                             \
   } while (0)
 
+// NVTX ranges around the phases of a call (header-only NVTX v3: no library, no cost when
+// no tool is attached)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
+
 int map_err(cudaError_t e) {
   if (e == cudaErrorMemoryAllocation) return ZZ_ERR_NOMEM;
   return ZZ_ERR_CUDA;
@@ -254,6 +262,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   if (!c->e0) {
     cudaEventCreate(&c->e0); cudaEventCreate(&c->e1); cudaEventCreate(&c->e2); cudaEventCreate(&c->e3);
   }
+  Range r_call("zz_tgevc");
   CK(cudaEventRecord(c->e0, st));
   int launches = 0;
   // ---- a1: structure scan (one host sync; none when S is on the host) ----
@@ -838,6 +847,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   };
   // (not with per-launch timing: the roofline pass measures plain stream launches)
   const bool use_graph = c->graphs && !hs && n_sel > 0 && !c->timing;
+  nvtxRangePushA(use_graph ? "zz.wavefront (graph)" : "zz.wavefront");
   if (use_graph) {
     // the plan's identity: sizes, modes, every pointer the launches use, and the host tables
     uint64_t key = 1469598103934665603ull;
@@ -899,6 +909,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   } else {
     if (int r = wavefront()) return r;
   }
+  nvtxRangePop();
   CK(cudaEventRecord(c->e2, st));
   // ---- a7 consistency and normalisation ----
   CK(launch_normalize(m, n_sel, M, X, ldx, cse, P, exp_tmp, rec_tmp, st));
@@ -1109,6 +1120,7 @@ int tgevc_sharded(Context* c, int m, const double* S, long long lds, const doubl
                   const int* select, double* X, long long ldx, int* cse, const double* Sh = nullptr,
                   long long ldsh = 0, const double* Th = nullptr, long long ldth = 0) {
   cudaStream_t st = c->stream;
+  Range r_call("zz_tgevc (sharded)");
   const NcclApi* api = c->comm ? nccl_api() : nullptr;
   if (c->comm && !api) return ZZ_ERR_NCCL;
   const int P = (c->nranks > 1) ? c->nranks : c->shard_P;
@@ -1182,6 +1194,7 @@ int tgevc_sharded(Context* c, int m, const double* S, long long lds, const doubl
   }
   if (r) return r;
   // ---- gather: pack the upper parts (rows 0 .. r_c) of the local columns ----
+  Range r_gather("zz.gather");
   auto region = [&](int q, std::vector<long long>* off) -> long long {   // bytes of shard q's buffer
     long long o = 0;
     if (off) off->resize(cols[q].size());
