@@ -133,6 +133,15 @@ int zz_set_tile(int mb);
  * Not used by the host-staged or collective paths.  Returns 0 or -103. */
 int zz_set_graphs(int on);
 
+/* Warps per diagonal-solve task (DESIGN.md s.6 "Teams"): the tile's 8-row blocks of a task's
+ * columns are split into W contiguous ranges, one per warp; the chain of blocks runs through
+ * the warps and every warp applies each solved block to its own rows with the same
+ * instructions, so results are bitwise independent of W.  0 (default) = one warp per task
+ * (measured fastest); -1 = as many warps per task as keep the step's tasks in one wave over
+ * the SMs; W in {1, 2, 3, 4, 6, 8, 12, 16} forces W where it divides the kernel's warps per
+ * CTA and the shared memory allows (otherwise 1).  Returns 0, -1 or -103. */
+int zz_set_diag_team(int w);
+
 /* Per-kernel timing of the robust update with CUDA events (0 off, 1 on): fills
  * zz_info_t.ms_update.  Adds an event pair per step; used by bench.py for the roofline. */
 int zz_set_timing(int on);

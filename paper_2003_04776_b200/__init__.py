@@ -30,7 +30,7 @@ STATUS = {
     -108: "shard emulation not allowed here",
 }
 
-EXPORTS = ["zz_get_unique_id", "zz_init", "zz_set_shard", "zz_shard_columns", "zz_set_stream", "zz_set_tile", "zz_set_graphs", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left", "zz_ztgevc",
+EXPORTS = ["zz_get_unique_id", "zz_init", "zz_set_shard", "zz_shard_columns", "zz_set_stream", "zz_set_tile", "zz_set_graphs", "zz_set_diag_team", "zz_set_timing", "zz_set_fusion", "zz_set_lookahead", "zz_tgevc", "zz_tgevc_host", "zz_tgevc_back", "zz_tgevc_left", "zz_ztgevc",
            "zz_count_columns", "zz_partition", "zz_last_info", "zz_finalize", "zz_status_string"]
 
 
@@ -121,6 +121,7 @@ def load(build_if_missing=True):
         "zz_set_tile": ([ci], ci),
         "zz_set_timing": ([ci], ci),
         "zz_set_graphs": ([ci], ci),
+        "zz_set_diag_team": ([ci], ci),
         "zz_set_fusion": ([ci], ci),
         "zz_set_lookahead": ([ci], ci),
         "zz_tgevc": ([ci, vp, ci, vp, ci, vp, vp, ci, vp], ci),
@@ -220,6 +221,12 @@ def set_lookahead(mode):
 def set_graphs(on):
     """CUDA-graph capture and replay of the wavefront (include/zz.h zz_set_graphs)."""
     _check(load().zz_set_graphs(1 if on else 0), "zz_set_graphs")
+
+
+def set_diag_team(w=0):
+    """Warps per diagonal-solve task (include/zz.h zz_set_diag_team; 0 = automatic).
+    Results are bitwise independent of it."""
+    _check(load().zz_set_diag_team(int(w)), "zz_set_diag_team")
 
 
 def set_timing(on):

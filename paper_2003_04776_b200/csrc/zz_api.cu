@@ -69,6 +69,8 @@ struct Context {
   // lookahead (zz_set_lookahead): the chain of solves runs on a high-priority stream beside
   // the bulk of the previous group's update (DESIGN.md s.6 "Lookahead"); 1 = automatic
   int lookahead = 1;
+  // warps per diagonal-solve task (zz_set_diag_team): 0 = automatic
+  int diag_team = 0;
   cudaStream_t hi = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::vector<cudaEvent_t> ev_la;
@@ -644,6 +646,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.P = P;
       d2.P.sY = sY_set[gpar];
       d2.pack = la;
+      d2.team_w = c->diag_team;
       d2.nY_in = dp.nY_in;
       d2.Wout = Wout;
       d2.grp_slot = -1;
@@ -856,7 +859,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       for (size_t i = 0; i < bytes; ++i) key = (key ^ q[i]) * 1099511628211ull;
     };
     const long long sc[] = {m, mb, n_sel, M, fusion, (long long)la, (long long)c->timing, (long long)vec, ldsu, ldtu,
-                            ldx, nb, n_items};
+                            ldx, nb, n_items, (long long)c->diag_team};
     mix(sc, sizeof(sc));
     const void* ptrs[] = {Su, Tu, X, c->colf.p, c->coli.p, c->items.p, c->tiles.p, c->rows.p, c->blks.p,
                           c->state.p, c->seg.p, c->norms.p, c->W.p, c->status.p, c->egrp.p, c->nYb.p, c->sYb.p,
@@ -1385,6 +1388,13 @@ int zz_set_lookahead(int mode) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (mode < 0 || mode > 2) return -1;
   g_ctx->lookahead = mode;
+  return 0;
+}
+
+int zz_set_diag_team(int w) {
+  if (!g_ctx) return ZZ_ERR_NOCTX;
+  if (!(w == -1 || w == 0 || w == 1 || w == 2 || w == 3 || w == 4 || w == 6 || w == 8 || w == 12 || w == 16)) return -1;
+  g_ctx->diag_team = w;
   return 0;
 }
 

@@ -40,7 +40,7 @@ constexpr int kPad3 = 32;      // zero double2 padding after the packed tile
 __device__ __forceinline__ int poff3(int j) { return j * (j + 3) / 2; }
 
 __device__ __forceinline__ double pow2k(int k) { return __hiloint2double((k + 1023) << 20, 0); }
-__device__ __forceinline__ double scale2_slow3(double x, int k) {
+__device__ __noinline__ double scale2_slow3(double x, int k) {
   while (k < -1022) { x *= 0x1p-1022; k += 1022; }
   return x * pow2k(k);
 }
@@ -56,28 +56,98 @@ struct Sm3 {
   double2* ST;     // packed tile: (S_ij, T_ij) at poff3(j) + i, rows i <= j + 1
   double2* cm;     // per row j: max |S_ij|, |T_ij| over the tile rows above j's block (R6)
   double2* tau;    // per block b: max over rows i < s_b of the sums over the block's rows
+  double2* bn;     // per block b: (||S_bb||_inf, ||T_bb||_inf) of the block's diagonal sub-block
   int* bs;         // block b = rows [bs[b], bs[b+1]); bs[b] = 8b - (row 8b is a 2x2 bottom)
-  double* slab;    // per warp: the current block's rows, [9 slots][8 columns]
-  double* pslab;   // per warp: prepared pivots of the block's 1x1 rows, [9][8][8]
+  unsigned char* teams;   // per team of warps: team_bytes(W, nblk) (see Team)
+  double* ptab;           // per warp: pivot table (G stage 1; the substitution's prepared pivots)
   signed char* fl; // row flags
 };
 
-__host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ __forceinline__ size_t smem3(int nt) {
-  return a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3)) + a16(sizeof(double2) * (size_t)nt) +
-         a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(sizeof(double) * 16 * 72) + a16(sizeof(double) * 16 * 576) + a16((size_t)nt);
+// One solved block as its owner warp publishes it to the other warps of its team.
+struct Pub {
+  double x[72];        // [9 slots][8 columns]: the block's rows (the owner's slab), after all
+                       // of the block's scalings
+  double bound[8];     // per column: running bound of the pending rows after the block
+  int kseg[8], eu[8];  // per column: the block's two segment scalings (in this order)
+  int ex[8];           // per column: exponent of the segment after the block (relative to e_pend)
+  int flag;            // 2 gen: published; 2 gen - 1: the owner asks for the pending maximum
+  int cnt;             // warps that answered the request
+  int pad[2];
+};
+static_assert(sizeof(Pub) % 16 == 0, "Pub alignment");
+
+// Per team: the publication records (one per block; W = 1: one, the warp's slab), the
+// prepared pivots of the slow path (only the warp solving the current block uses them) and
+// two reduction areas (initial bound; segment norms).
+__host__ __device__ __forceinline__ size_t team_bytes(int W, int nblk) {
+  return sizeof(Pub) * (size_t)(W == 1 ? 1 : nblk) + sizeof(double) * 8 * (size_t)W +
+         sizeof(double) * 16 * (size_t)W + sizeof(double) * 8 * (size_t)W;
 }
-__device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt) {
+constexpr size_t kPtabBytes = sizeof(double) * 576;   // per warp: pivot table [9][8][8]
+
+__host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ __forceinline__ size_t smem3(int nt, int nteams, size_t tb, int nwarps) {
+  return a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3)) + a16(sizeof(double2) * (size_t)nt) +
+         a16(sizeof(double2) * 17) + a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(tb) * nteams +
+         kPtabBytes * nwarps + a16((size_t)nt);
+}
+__device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt, int nteams, size_t tb, int nwarps) {
   Sm3 s;
   size_t o = 0;
   s.ST = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3));
   s.cm = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * (size_t)nt);
   s.tau = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * 17);
+  s.bn = reinterpret_cast<double2*>(base + o); o += a16(sizeof(double2) * 17);
   s.bs = reinterpret_cast<int*>(base + o); o += a16(sizeof(int) * 18);
-  s.slab = reinterpret_cast<double*>(base + o); o += a16(sizeof(double) * 16 * 72);
-  s.pslab = reinterpret_cast<double*>(base + o); o += a16(sizeof(double) * 16 * 576);
+  s.teams = base + o; o += a16(tb) * nteams;
+  s.ptab = reinterpret_cast<double*>(base + o); o += kPtabBytes * nwarps;
   s.fl = reinterpret_cast<signed char*>(base + o);
   return s;
+}
+
+// A team: W warps solving one task together (warp w owns a contiguous range of blocks).
+struct Team {
+  int W, w;        // team size, this warp's index in it
+  int bar;         // named barrier of the team (W > 1)
+  int gen;         // task + 1: the generation of the publication flags
+  Pub* pub;
+  double* pslab;   // this warp's pivot table [9][8][8]
+  double* red0;    // [W][8] initial bound
+  double* red1;    // [W][8][2] segment norms
+  double* red2;    // [W][8] pending maxima (answers to an owner's request)
+};
+
+#ifdef ZZ_VARIANT_TRACE
+__device__ long long g_trace[256];
+#define ZZ_TR(i) do { if (blockIdx.x == 0 && tm.gen == 1 && lane == 0) g_trace[(i)] = clock64(); } while (0)
+#define ZZ_TR0() do { if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[180] = clock64(); } while (0)
+#else
+#define ZZ_TR(i) do { } while (0)
+#define ZZ_TR0() do { } while (0)
+#endif
+
+__device__ __forceinline__ void team_sync(const Team& tm) {
+  if (tm.W > 1) asm volatile("bar.sync %0, %1;" ::"r"(tm.bar), "r"(tm.W * 32) : "memory");
+}
+// publication flag: release by the owner (after a __syncwarp over the writes), acquire by a reader
+__device__ __forceinline__ void pub_release(int* flag, int gen) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(flag)), "r"(gen)
+               : "memory");
+}
+__device__ __forceinline__ int ld_relaxed(const int* flag) {
+  int v;
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(flag)) : "memory");
+  return v;
+}
+// (spins use relaxed loads and one acquire fence once the awaited value is seen)
+// wait until *flag == v1 (or, if v0 != 0, == v0); returns the value seen (all lanes)
+__device__ __forceinline__ int pub_wait(const int* flag, int v1, int lane, int v0 = 0) {
+  int v;
+  do {   // warp-uniform: every lane loads the same word (one broadcast load)
+    v = ld_relaxed(flag);
+  } while (v != v1 && (v0 == 0 || v != v0));
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
+  return v;
 }
 
 // ------------------------------------------------------------------------------------
@@ -209,11 +279,358 @@ __device__ __forceinline__ double pending_max(const Seg<G>& s, int rot, int t, i
 }
 
 // ------------------------------------------------------------------------------------
+// Fast block solve (the tile's critical path): x = D^{-1} y for the rows of one
+// block, D = beta S_bb - alpha T_bb, through the block-local inverse G = D^{-1}.  G
+// depends on the column's eigenvalue and the staged tile only, not on y, so its rows are
+// formed with independent instructions; the dependency chain through a block is then one
+// short matrix-vector product instead of a row-by-row substitution.  Lanes: a real column's
+// lane t forms the G rows of slots t, t + 4 (and 8 for t = 0); a complex pair's eight lanes
+// u = 4 comp + t the row of slot u (and 8 for u = 0).  A row of G is formed right-looking:
+// g_J = acc_J D_JJ^{-1}, then acc_l -= g_J D_Jl for l > J; a 2x2 diagonal block by its
+// explicit inverse.  Pivots are the protected ones of the substitution (R8: |d| < smin ->
+// smin).  The result is used only if it cannot overflow and G is well conditioned relative
+// to D: for every row, (sum_J |G_qJ|) max|y| <= 2^1000 and (sum_J |G_qJ|) ||D_bb|| <= 2^40
+// (an Inf or NaN fails both); the caller then takes the protected substitution
+// (ProtectDivision / ProtectUpdate) for the column instead.  Returns that verdict for this
+// lane's rows; xr/xi receive the lane's solution rows.
+// ------------------------------------------------------------------------------------
+// power of two sc with sc ||D_bb|| in [1/2, 1) (clamped to [2^-500, 2^500]): G is formed for
+// sc D (no subnormal entries at any scale of the pencil; results equivariant under
+// (S, T) -> 2^k (S, T)) and x = sc (G' y)
+__device__ __forceinline__ double gscale(double dn) {
+  int pe;
+  frexp(dn, &pe);
+  return (dn > 0.0) ? pow2k(-max(-500, min(500, pe))) : 1.0;
+}
+
+struct GRows {
+  double ar[9], ai[9], br[9];                     // rows A (complex for pairs) and B (real)
+  double cr7, ci7, cr8, ci8;                      // row C: slots 7 and 8
+};
+
+// Stage 1 of gprep_block: the inverses of the diagonal 1x1 / 2x2 blocks of one column (R8
+// perturbation as in the substitution), written to the warp's pivot table ptab[slot][column][4]:
+// 1x1 slot J: (1/d) at [J][0..1]; 2x2 block (J, J+1): real -- inv at [J][0..3] (row-major);
+// pair -- inv row 0 at [J][0..3], row 1 at [J+1][0..3] (complex).  A rolled loop (compact code:
+// the diagonal solve is bound by instruction fetch when its code is unrolled).
+template <bool PAIR>
+__device__ __noinline__ void gpiv_block(const Sm3& sm, int r0, int q0, int qe, double a, double b, double beta,
+                                        double ab, int u, int col, double* ptab) {
+  const int nl = PAIR ? 8 : 4;
+#pragma unroll 1
+  for (int J = u; J < qe; J += nl) {
+    if (J < q0) continue;
+    const int j = r0 + J;
+    const int fJ = sm.fl[j];
+    if (fJ == kRowBot2) continue;
+    double* pt = ptab + (J * 8 + col) * 4;
+    if (fJ == kRowTop2) {
+      const double2 e00 = sm.ST[poff3(j) + j], e10 = sm.ST[poff3(j) + j + 1];
+      const double2 e01 = sm.ST[poff3(j + 1) + j], e11 = sm.ST[poff3(j + 1) + j + 1];
+      const double maxs = dmaxd(dmaxd(fabs(e00.x), fabs(e10.x)), dmaxd(fabs(e01.x), fabs(e11.x)));
+      const double maxt = dmaxd(dmaxd(fabs(e00.y), fabs(e01.y)), fabs(e11.y));
+      const double smin = dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, maxs), __dmul_rn(ab, maxt))), kSmlnum);
+      const cpx d00 = mkc(__fma_rn(-a, e00.y, __dmul_rn(beta, e00.x)), -b * e00.y);
+      const cpx d01 = mkc(__fma_rn(-a, e01.y, __dmul_rn(beta, e01.x)), -b * e01.y);
+      const double d10 = __dmul_rn(beta, e10.x);
+      const cpx d11 = mkc(__fma_rn(-a, e11.y, __dmul_rn(beta, e11.x)), -b * e11.y);
+      const double pv = dmaxd(dmaxd(n1(d00), n1(d01)), dmaxd(fabs(d10), n1(d11)));
+      // the block scaled by a power of two sc ~ 1/pv (D^-1 = sc (sc D)^-1): no overflow or
+      // underflow at any scale, so results are equivariant under (S, T) -> 2^k (S, T)
+      int pe;
+      frexp(pv, &pe);
+      const double sc = pow2k(-max(-1000, min(1000, pe)));
+      const cpx s00 = mkc(d00.re * sc, d00.im * sc), s11 = mkc(d11.re * sc, d11.im * sc);
+      const cpx s01 = mkc(d01.re * sc, d01.im * sc);
+      const double s10 = d10 * sc;
+      if (!PAIR) {
+        double det = fma(s00.re, s11.re, -(s01.re * s10));
+        if (fabs(det) < smin * sc) det = smin * sc;
+        const double rd = __drcp_rn(det) * sc;
+        pt[0] = s11.re * rd;
+        pt[1] = -s01.re * rd;
+        pt[2] = -s10 * rd;
+        pt[3] = s00.re * rd;
+      } else {
+        cpx det = csubx(cmulx(s00, s11), mkc(s01.re * s10, s01.im * s10));
+        if (n1(det) < smin * sc) det = mkc(smin * sc, 0.0);
+        cpx rd;   // 1 / det (Smith)
+        if (fabs(det.re) >= fabs(det.im)) {
+          const double sr = det.im * __drcp_rn(det.re), r = __drcp_rn(fma(det.im, sr, det.re));
+          rd = mkc(r, -sr * r);
+        } else {
+          const double sr = det.re * __drcp_rn(det.im), r = __drcp_rn(fma(det.re, sr, det.im));
+          rd = mkc(sr * r, -r);
+        }
+        rd = mkc(rd.re * sc, rd.im * sc);
+        const cpx i00 = cmulx(s11, rd), i11 = cmulx(s00, rd);
+        const cpx i01 = cmulx(mkc(-s01.re, -s01.im), rd), i10 = mkc(-s10 * rd.re, -s10 * rd.im);
+        pt[0] = i00.re; pt[1] = i00.im; pt[2] = i01.re; pt[3] = i01.im;
+        pt[32] = i10.re; pt[33] = i10.im; pt[34] = i11.re; pt[35] = i11.im;   // slot J+1
+      }
+    } else {
+      const double2 dd = sm.ST[poff3(j) + j];
+      cpx d = mkc(__fma_rn(-a, dd.y, __dmul_rn(beta, dd.x)), __dmul_rn(-b, dd.y));
+      const double smin =
+          dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, fabs(dd.x)), __dmul_rn(ab, fabs(dd.y)))), kSmlnum);
+      if (n1(d) < smin) d = mkc(smin, 0.0);
+      if (!PAIR) {
+        pt[0] = __drcp_rn(d.re);
+      } else if (fabs(d.re) >= fabs(d.im)) {
+        const double sr = d.im * __drcp_rn(d.re), r = __drcp_rn(fma(d.im, sr, d.re));
+        pt[0] = r;
+        pt[1] = -sr * r;
+      } else {
+        const double sr = d.re * __drcp_rn(d.im), r = __drcp_rn(fma(d.re, sr, d.im));
+        pt[0] = sr * r;
+        pt[1] = -r;
+      }
+    }
+  }
+}
+
+// Stage 2: this lane's rows of G = D^{-1} for the block (slots [q0, qe)), right-looking:
+// g_J = acc_J D_JJ^{-1} (from the pivot table), acc_l -= g_J D_Jl for l > J.
+template <bool PAIR>
+__device__ __forceinline__ void gprep_block(const Sm3& sm, int g8, int q0, int qe, int nt, double a, double b,
+                                            double beta, double ab, int u, int col, double* ptab, GRows& gr) {
+  const int r0 = g8 - 1;                          // row of slot 0
+  __syncwarp();   // the pivot table (gpiv_block) is complete
+  // entry (slot J, slot l) at sm.ST[off[l] + J]; columns past the tile are clamped (their
+  // entries only feed accumulators of slots >= qe, which are never read)
+  int off[9];
+#pragma unroll
+  for (int l = 0; l < 9; ++l) off[l] = poff3(min(r0 + l, nt - 1)) + r0;
+  const int qA = u, qB = PAIR ? 99 : u + 4;       // slots of this lane's G rows (C: slot 8)
+  const bool hasC = (u == 0) && qe == 9;
+  double (&ar)[9] = gr.ar, (&ai)[9] = gr.ai, (&br)[9] = gr.br;
+  double &cr7 = gr.cr7, &ci7 = gr.ci7, &cr8 = gr.cr8, &ci8 = gr.ci8;
+  cr7 = 0.0; ci7 = 0.0; cr8 = 1.0; ci8 = 0.0;
+#pragma unroll
+  for (int J = 0; J < 9; ++J) {
+    ar[J] = (J == qA) ? 1.0 : 0.0;
+    ai[J] = 0.0;
+    br[J] = (J == qB) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int J = 0; J < 9; ++J) {
+    if (J < q0 || J >= qe) continue;
+    const int fJ = sm.fl[r0 + J];
+    if (fJ == kRowBot2) continue;                 // solved with the top row of its block
+    const double* pt = ptab + (J * 8 + col) * 4;
+    if (J < 8 && fJ == kRowTop2) {
+      // ---- 2x2 diagonal block (J, J+1): [g_J, g_J+1] = [acc_J, acc_J+1] inv ----
+      if (!PAIR) {
+        const double2 p01 = *reinterpret_cast<const double2*>(pt), p23 = *reinterpret_cast<const double2*>(pt + 2);
+        const double i00 = p01.x, i01 = p01.y, i10 = p23.x, i11 = p23.y;
+#define ZZ_ROW2R(x0, x1)                                              \
+  {                                                                   \
+    const double g0_ = fma(x1, i10, x0 * i00), g1_ = fma(x1, i11, x0 * i01); \
+    x0 = g0_;                                                         \
+    x1 = g1_;                                                         \
+  }
+        ZZ_ROW2R(ar[J], ar[J + 1]);
+        if (J >= 3) ZZ_ROW2R(br[J], br[J + 1]);
+        if (J == 7 && hasC) ZZ_ROW2R(cr7, cr8);
+#undef ZZ_ROW2R
+      } else {
+        const double2 q0v = *reinterpret_cast<const double2*>(pt), q1v = *reinterpret_cast<const double2*>(pt + 2);
+        const double2 q2v = *reinterpret_cast<const double2*>(pt + 32), q3v = *reinterpret_cast<const double2*>(pt + 34);
+        const cpx i00 = mkc(q0v.x, q0v.y), i01 = mkc(q1v.x, q1v.y), i10 = mkc(q2v.x, q2v.y), i11 = mkc(q3v.x, q3v.y);
+#define ZZ_ROW2C(r0v, i0v, r1v, i1v)                                                        \
+  {                                                                                         \
+    const double g0r = fma(-i1v, i10.im, fma(r1v, i10.re, fma(-i0v, i00.im, r0v * i00.re))); \
+    const double g0i = fma(i1v, i10.re, fma(r1v, i10.im, fma(i0v, i00.re, r0v * i00.im)));   \
+    const double g1r = fma(-i1v, i11.im, fma(r1v, i11.re, fma(-i0v, i01.im, r0v * i01.re))); \
+    const double g1i = fma(i1v, i11.re, fma(r1v, i11.im, fma(i0v, i01.re, r0v * i01.im)));   \
+    r0v = g0r; i0v = g0i; r1v = g1r; i1v = g1i;                                             \
+  }
+        ZZ_ROW2C(ar[J], ai[J], ar[J + 1], ai[J + 1]);
+        if (J == 7 && hasC) ZZ_ROW2C(cr7, ci7, cr8, ci8);
+#undef ZZ_ROW2C
+      }
+#pragma unroll
+      for (int l = 0; l < 9; ++l) {   // constant trip count: unrolled after J is
+        if (l >= J + 2) {
+          const double2 f0 = sm.ST[off[l] + J], f1 = sm.ST[off[l] + J + 1];
+          const double D0r = __fma_rn(-a, f0.y, __dmul_rn(beta, f0.x)), D1r = __fma_rn(-a, f1.y, __dmul_rn(beta, f1.x));
+          if (!PAIR) {
+            ar[l] = fma(-ar[J + 1], D1r, fma(-ar[J], D0r, ar[l]));
+            if (J >= 3) br[l] = fma(-br[J + 1], D1r, fma(-br[J], D0r, br[l]));
+          } else {
+            const double D0i = -b * f0.y, D1i = -b * f1.y;
+            ar[l] = fma(ai[J + 1], D1i, fma(-ar[J + 1], D1r, fma(ai[J], D0i, fma(-ar[J], D0r, ar[l]))));
+            ai[l] = fma(-ar[J + 1], D1i, fma(-ai[J + 1], D1r, fma(-ar[J], D0i, fma(-ai[J], D0r, ai[l]))));
+          }
+        }
+      }
+    } else {
+      // ---- 1x1 pivot ----
+      if (!PAIR) {
+        const double r = pt[0];
+        ar[J] *= r;
+        if (J >= 3) br[J] *= r;
+        if (J == 7 && hasC) cr7 *= r;
+        if (J == 8 && hasC) cr8 *= r;
+      } else {
+        const double2 rv = *reinterpret_cast<const double2*>(pt);
+        const cpx rd = mkc(rv.x, rv.y);
+#define ZZ_MULR(vr_, vi_)                                                            \
+  {                                                                                 \
+    const double nr_ = fma(-vi_, rd.im, vr_ * rd.re), ni_ = fma(vi_, rd.re, vr_ * rd.im); \
+    vr_ = nr_;                                                                      \
+    vi_ = ni_;                                                                      \
+  }
+        ZZ_MULR(ar[J], ai[J]);
+        if (J == 7 && hasC) ZZ_MULR(cr7, ci7);
+        if (J == 8 && hasC) ZZ_MULR(cr8, ci8);
+#undef ZZ_MULR
+      }
+#pragma unroll
+      for (int l = 0; l < 9; ++l) {
+        if (l >= J + 1) {
+          const double2 f = sm.ST[off[l] + J];
+          const double Dr = __fma_rn(-a, f.y, __dmul_rn(beta, f.x));
+          if (!PAIR) {
+            ar[l] = fma(-ar[J], Dr, ar[l]);
+            if (J >= 3) br[l] = fma(-br[J], Dr, br[l]);
+            if (J == 7 && l == 8 && hasC) cr8 = fma(-cr7, Dr, cr8);
+          } else {
+            const double Di = -b * f.y;
+            ar[l] = fma(ai[J], Di, fma(-ar[J], Dr, ar[l]));
+            ai[l] = fma(-ar[J], Di, fma(-ai[J], Dr, ai[l]));
+            if (J == 7 && l == 8 && hasC) {
+              const double nr = fma(ci7, Di, fma(-cr7, Dr, cr8));
+              ci8 = fma(-cr7, Di, fma(-ci7, Dr, ci8));
+              cr8 = nr;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();   // the pivot table is reused (slow path, next block)
+}
+
+// x = G y for this lane's rows and the overflow / conditioning verdict (see gprep_block)
+template <bool PAIR>
+__device__ __forceinline__ bool gapply_block(const GRows& gr, const double* wslab, int q0, int qe, double dn,
+                                             double sc, int team, int u, double (&xr)[3], double (&xi)[3]) {
+  const int qB = PAIR ? 99 : u + 4, qA = u;
+  const bool hasC = (u == 0) && qe == 9;
+  const int pt = PAIR ? (team & ~1) : team;       // slab column of Re (Im at pt + 1)
+  const double (&ar)[9] = gr.ar, (&ai)[9] = gr.ai, (&br)[9] = gr.br;
+  const double cr7 = gr.cr7, ci7 = gr.ci7, cr8 = gr.cr8, ci8 = gr.ci8;
+  // ---- x = G y (sources in ascending slot order), row sums of |G| ----
+  double ymax = 0.0, sA = 0.0, sB = 0.0;
+  double xar = 0.0, xai = 0.0, xbr = 0.0, xcr = 0.0, xci = 0.0;
+#pragma unroll
+  for (int J = 0; J < 9; ++J) {
+    if (J >= q0 && J < qe) {
+      const double yr = wslab[J * 8 + pt], yi = PAIR ? wslab[J * 8 + pt + 1] : 0.0;
+      ymax = dmaxd(ymax, PAIR ? dmaxd(fabs(yr), fabs(yi)) : fabs(yr));
+      if (!PAIR) {
+        xar = fma(ar[J], yr, xar);
+        sA += fabs(ar[J]);
+        if (J >= 3) {
+          xbr = fma(br[J], yr, xbr);
+          sB += fabs(br[J]);
+        }
+      } else {
+        xar = fma(-ai[J], yi, fma(ar[J], yr, xar));
+        xai = fma(ai[J], yr, fma(ar[J], yi, xai));
+        sA += fabs(ar[J]) + fabs(ai[J]);
+      }
+      if (J == 7 && hasC) {
+        xcr = fma(-ci7, yi, fma(cr7, yr, xcr));
+        xci = fma(ci7, yr, fma(cr7, yi, xci));
+      }
+      if (J == 8 && hasC) {
+        xcr = fma(-ci8, yi, fma(cr8, yr, xcr));
+        xci = fma(ci8, yr, fma(cr8, yi, xci));
+      }
+    }
+  }
+  const double sC = (qe == 9) ? (fabs(cr7) + fabs(ci7) + fabs(cr8) + fabs(ci8)) : 0.0;
+  const double yb = PAIR ? 2.0 * ymax : ymax;
+  const double lim = 0x1p1000 / sc;   // |x| = sc |G' y| <= 2^1000
+  bool ok = true;
+  if (qA >= q0 && qA < qe) ok = ok && (sA * yb <= lim) && (sA * dn <= 0x1p40);
+  if (!PAIR && qB < qe) ok = ok && (sB * yb <= lim) && (sB * dn <= 0x1p40);
+  if (hasC) ok = ok && (sC * yb <= lim) && (sC * dn <= 0x1p40);
+  xr[0] = xar * sc; xi[0] = xai * sc;
+  xr[1] = xbr * sc; xi[1] = 0.0;
+  xr[2] = xcr * sc; xi[2] = xci * sc;
+  return ok;
+}
+
+// max |value| over the rows [r0, r1) of the column held by this warp (position p holds group
+// (p - rot) mod G; pairs: over both components)
+template <int G, bool PAIR>
+__device__ __forceinline__ double range_max(const Seg<G>& s, int rot, int t, int r0, int r1) {
+  double m = 0.0;
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = (q - rot + G) % G;
+    const int r = 8 * g + 2 * t;
+    if (r >= r0 && r < r1) m = fmax(m, fabs(s.y[q][0]));
+    if (r + 1 >= r0 && r + 1 < r1) m = fmax(m, fabs(s.y[q][1]));
+  }
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  if (PAIR) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  return m;
+}
+
+// DMMA update of the groups g in [gmin, k) held by this warp (position q holds group
+// top - (G-1-q)) with the solution of block k: Y(8 columns x 8 rows) += A (8 x 4) . [S | T]^T
+// over the block's source rows 8k + 4 kk + t (kk = 0, 1) and its straddling top row 8k - 1
+// (kk = 2) -- the instruction sequence of the block's owner, for every warp.
+template <int G>
+__device__ __forceinline__ void dmma_block(Seg<G>& s, int top, int k, int gmin, bool st, const Sm3& sm, int nt,
+                                           int t, int team, const double (&aS)[3], const double (&aT)[3]) {
+  const int g8 = 8 * k;
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int g = top - (G - 1 - q);
+    if (g >= gmin && g < k) {
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        if (kk == 2 && !st) continue;
+        const int src0 = (kk < 2) ? g8 + 4 * kk : g8 - 4;
+        const double2 v = sm.ST[poff3(min(src0 + t, nt - 1)) + 8 * g + team];
+        dmma3(s.y[q][0], s.y[q][1], aS[kk], v.x);
+        dmma3(s.y[q][0], s.y[q][1], aT[kk], v.y);
+      }
+    }
+  }
+}
+
+// A fragments of block k's update from its publication: lane (team, t) holds its column's
+// coefficients [-beta x | alpha x] for source row src0 + t (the owner forms the same values
+// from its registers).
+template <bool PAIR>
+__device__ __forceinline__ void pub_frags(const double* x, const Sm3& sm, int k, double a, double b, double beta,
+                                          int team, int t, int comp, double (&aS)[3], double (&aT)[3]) {
+  const int g8 = 8 * k, e0 = sm.bs[k + 1];
+  const bool st = sm.bs[k] < g8;
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    const int slot = (kk < 2) ? 1 + 4 * kk + t : 0;
+    const bool in = (kk < 2) ? (g8 + 4 * kk + t < e0) : (st && t == 3);
+    const double v = in ? x[slot * 8 + team] : 0.0;
+    const double o = (PAIR && in) ? x[slot * 8 + (team ^ 1)] : 0.0;
+    const double xr = PAIR ? (comp ? o : v) : v, xi = PAIR ? (comp ? v : o) : 0.0;
+    aS[kk] = -(beta * v);
+    aT[kk] = PAIR ? (comp ? (a * xi + b * xr) : (a * xr - b * xi)) : a * xr;
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // One task: 8 real columns (PAIR = false) or 4 complex pairs (PAIR = true) of tile I.
 // ------------------------------------------------------------------------------------
 template <int G, bool PAIR>
-__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, double* wslab,
-                           double* pslab) {
+__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, const Team& tm) {
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
@@ -237,10 +654,23 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     if (tip) tipr = P.col_r[c0] - p.t0;
   }
   const double ab = __dadd_rn(fabs(a), fabs(b));
+  // pending exponent of the column (read before any warp of the team writes the new one)
+  const int ep = (valid && !tip) ? P.e_pend[c] : 0;
   const int nt = p.nt;
   const int pbase = lane & ~3;           // first lane of this column's team
   constexpr int CUR = G - 1, PRV = G - 2;
 
+  // ---- the team (W warps per task; W = 1: one warp): warp w owns the blocks [lo, hi) and
+  // their rows [rlo, rhi); the chain of blocks runs bottom-up through the warps W-1, ..., 0.
+  // Every warp applies the published solution of each block below its range to its rows
+  // (the same DMMA instructions on the same operands as the block's owner would issue), so
+  // the arithmetic of a column does not depend on W.  Group lo-1 is kept as well when it
+  // holds the top row of a 2x2 block that straddles into block lo. ----
+  const int W = tm.W, w = tm.w;
+  const int lo = (w * nblk) / W, hi = ((w + 1) * nblk) / W;
+  const int rlo = sm.bs[lo], rhi = sm.bs[hi];
+  const int gmin = (lo > 0 && rlo < 8 * lo) ? lo - 1 : lo;
+  Pub* const pub = tm.pub;
   // ---- right-hand side (tips start from zero) ----
   Seg<G> s;
   {
@@ -249,16 +679,76 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int r = 8 * g + 2 * t;
-      s.y[g][0] = (ld && r < nt) ? xc[r] : 0.0;
-      s.y[g][1] = (ld && r + 1 < nt) ? xc[r + 1] : 0.0;
+      const bool mine = ld && g >= gmin && g < hi;
+      s.y[g][0] = (mine && r < nt) ? xc[r] : 0.0;
+      s.y[g][1] = (mine && r + 1 < nt) ? xc[r + 1] : 0.0;
     }
   }
   int rot = 0;
-  while (rot < G - nblk) { s.rotate(); ++rot; }   // group nblk-1 -> position G-1
+  while (rot < G - hi) { s.rotate(); ++rot; }   // group hi-1 -> position G-1
   int ex = 0;   // exponent of the segment relative to e_pend (stored = 2^ex true)
-  double bound = pending_max<G, PAIR>(s, rot, t, nt);   // running bound of max |pending|
+  // running upper bound of max |pending| (Alg. 3's y^): initially the exact maximum over
+  // the tile's rows (a max is exact and order-independent: the same for every W)
+  double bound = range_max<G, PAIR>(s, rot, t, rlo, rhi);
+  // the pivots of this warp's first block (the rcp chains of G's stage 1), formed before the
+  // chain reaches it (W > 1: while the warps below solve their blocks); the others in turn
+  int pre_blk = -1;
+  if (W > 1 && hi > lo) {
+    const int k = hi - 1, g8k = 8 * k;
+    const double2 bk = sm.bn[k];
+    const double sck = gscale(__dadd_rn(__dmul_rn(beta, bk.x), __dmul_rn(ab, bk.y)));
+    gpiv_block<PAIR>(sm, g8k - 1, sm.bs[k] - (g8k - 1), sm.bs[k + 1] - (g8k - 1), a * sck, b * sck, beta * sck, ab * sck,
+                     PAIR ? comp * 4 + t : t, PAIR ? (team & ~1) : team, tm.pslab);
+    pre_blk = k;
+  }
+  ZZ_TR(200 + w);
+  if (W > 1) {
+    if (t == 0) tm.red0[w * 8 + team] = bound;
+    team_sync(tm);
+    if (hi == nblk) {
+      bound = 0.0;
+      for (int v = 0; v < W; ++v) bound = dmaxd(bound, tm.red0[v * 8 + team]);
+    }
+    // the blocks below this warp's range: their scalings and updates, in the chain's order
+    for (int k = nblk - 1; k >= hi; --k) {
+      Pub& pk = pub[k];
+      const int v = pub_wait(&pk.flag, 2 * tm.gen, lane, 2 * tm.gen - 1);
+      ZZ_TR(k * 8 + 5);
+      const int k1 = pk.kseg[team];
+      if (k1 < 0) s.scale(k1);
+      if (v != 2 * tm.gen) {
+        // the owner asks for the exact maximum of the pending rows (after the block's
+        // in-block scaling): this warp's rows are all above block k
+        const double mx = range_max<G, PAIR>(s, rot, t, rlo, rhi);
+        if (t == 0) tm.red2[w * 8 + team] = mx;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicAdd(&pk.cnt, 1);
+        }
+        pub_wait(&pk.flag, 2 * tm.gen, lane);
+      }
+      const int k2 = pk.eu[team];
+      if (k2 < 0) s.scale(k2);
+      if (k > 0) {
+        double aS[3], aT[3];
+        pub_frags<PAIR>(pk.x, sm, k, a, b, beta, team, t, comp, aS, aT);
+        dmma_block<G>(s, hi - 1, k, gmin, sm.bs[k] < 8 * k, sm, nt, t, team, aS, aT);
+        // the top row of a block that straddles into block hi belongs to that block's owner
+        if (k == hi && sm.bs[k] < 8 * k && t == 3) s.y[G - 1][1] = 0.0;   // group hi-1 at position G-1
+      }
+      ZZ_TR(k * 8 + 6);
+    }
+    ZZ_TR(220 + w);
+    if (hi < nblk && hi > lo) {
+      bound = pub[hi].bound[team];
+      ex = pub[hi].ex[team];
+    }
+  }
 
-  for (int blk = nblk - 1; blk >= 0; --blk) {
+  for (int blk = hi - 1; blk >= lo; --blk) {
+    double* const wslab = pub[W == 1 ? 0 : blk].x;
+    double* const pslab = tm.pslab;
     const int s0 = sm.bs[blk], e0 = sm.bs[blk + 1];
     const int g8 = 8 * blk;
     const bool st = s0 < g8;             // row 8 blk - 1 (a 2x2 top) belongs to this block
@@ -274,6 +764,39 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     wslab[(2 + 2 * t) * 8 + team] = s.y[CUR][1];
     if (t == 3) wslab[team] = s.y[PRV][1];
     const int q0 = s0 - (g8 - 1);
+    __syncwarp();
+    // ---- fast path: the block-local inverse (gsolve_block); the tip's own block and
+    // columns whose check fails take the protected substitution below ----
+    ZZ_TR(blk * 8 + 0);
+    double xfr[3], xfi[3];
+    const double2 bnv = sm.bn[blk];
+    const double dn0 = __dadd_rn(__dmul_rn(beta, bnv.x), __dmul_rn(ab, bnv.y));
+    const double gsc = gscale(dn0), dn = dn0 * gsc;   // G is formed for gsc D (gscale)
+    const int u = PAIR ? comp * 4 + t : t;
+    if (blk != pre_blk)
+      gpiv_block<PAIR>(sm, g8 - 1, q0, e0 - (g8 - 1), a * gsc, b * gsc, beta * gsc, ab * gsc, u, PAIR ? (team & ~1) : team, pslab);
+    GRows gpre;
+    gprep_block<PAIR>(sm, g8, q0, e0 - (g8 - 1), nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u,
+                      PAIR ? (team & ~1) : team, pslab, gpre);
+    bool okc = gapply_block<PAIR>(gpre, wslab, q0, e0 - (g8 - 1), dn, gsc, team, u, xfr, xfi);
+#ifndef ZZ_VARIANT_NOTIP
+    okc = okc && !(tip && tipr >= s0 && tipr < e0);
+#endif
+#ifdef ZZ_VARIANT_NOFAST
+    okc = false;
+#endif
+    {   // one verdict per column (pair: both columns); every lane shuffles
+      int v = okc ? 1 : 0;
+      v &= __shfl_xor_sync(0xffffffffu, v, 1);
+      v &= __shfl_xor_sync(0xffffffffu, v, 2);
+      if (PAIR) v &= __shfl_xor_sync(0xffffffffu, v, 4);
+      okc = (v != 0) || !valid;
+    }
+    int kseg = 0;
+    ZZ_TR(blk * 8 + 1);
+    if (__any_sync(0xffffffffu, !okc)) {
+    const double bound0 = bound;
+    const int ex0 = ex;
     // pivots of the block's 1x1 rows, off the dependency chain: lane t prepares slots t,
     // t+4, t+8 of its column -- the perturbed pivot d (R8), its reciprocal (real) or Smith's
     // ratio and denominator (pair), and the ProtectDivision threshold (|w| <= thr: no scaling)
@@ -306,7 +829,6 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     }
     __syncwarp();
     int j = e0 - 1;
-    int kseg = 0;
     while (j >= s0) {
       const int q = j - (g8 - 1);
       const bool two = sm.fl[j] == kRowBot2;
@@ -429,20 +951,74 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       __syncwarp();
       j = qs - 1 + (g8 - 1);
     }
+    if (okc) {   // the substitution ran for other columns of the warp: keep the fast result
+      bound = bound0;
+      ex = ex0;
+      kseg = 0;
+    }
+    }   // protected substitution
+    ZZ_TR(blk * 8 + 2);
+    if (okc) {
+      const int qe = e0 - (g8 - 1);
+      const int pt = PAIR ? (team & ~1) : team;
+      double xm = 0.0;
+      if (u >= q0 && u < qe) {
+        wslab[u * 8 + pt] = xfr[0];
+        if (PAIR) wslab[u * 8 + pt + 1] = xfi[0];
+        xm = PAIR ? dmaxd(fabs(xfr[0]), fabs(xfi[0])) : fabs(xfr[0]);
+      }
+      if (!PAIR && u + 4 < qe) {
+        wslab[(u + 4) * 8 + team] = xfr[1];
+        xm = dmaxd(xm, fabs(xfr[1]));
+      }
+      if (u == 0 && qe == 9) {
+        wslab[64 + pt] = xfr[2];
+        if (PAIR) wslab[64 + pt + 1] = xfi[2];
+        xm = dmaxd(xm, PAIR ? dmaxd(fabs(xfr[2]), fabs(xfi[2])) : fabs(xfr[2]));
+      }
+      xnb = xm;
+    }
+    {   // max |x| over the block's rows of the column (fast result)
+      double xm = okc ? xnb : 0.0;
+      xm = dmaxd(xm, __shfl_xor_sync(0xffffffffu, xm, 1));
+      xm = dmaxd(xm, __shfl_xor_sync(0xffffffffu, xm, 2));
+      if (PAIR) xm = dmaxd(xm, __shfl_xor_sync(0xffffffffu, xm, 4));
+      if (okc) xnb = xm;
+    }
+    __syncwarp();
     // ---- the block's rows back to their owner lanes ----
     if (kseg < 0) s.scale(kseg);
     s.y[CUR][0] = wslab[(1 + 2 * t) * 8 + team];
     s.y[CUR][1] = wslab[(2 + 2 * t) * 8 + team];
     if (st && t == 3) s.y[PRV][1] = wslab[team];
     __syncwarp();
+    int eu = 0;
     if (blk > 0) {
       // ---- update of all rows above the block by DMMA (Alg. 3 on the in-tile panel) ----
       const double2 tv = sm.tau[blk];
       const double tt = __dadd_rn(__dmul_rn(beta, tv.x), __dmul_rn(ab, tv.y));
+      // ProtectUpdate: while the running bound of the pending rows keeps every column of the
+      // task below 2^1020 nothing scales; otherwise the exact maximum of the pending rows
+      // replaces the bound of every column (rows above this warp's range: asked from the warps
+      // that hold them, after the block's in-block scaling, which they apply first)
       double nb = fma(tt, xnb, bound);
-      if (__any_sync(0xffffffffu, !(nb <= 0x1p1020))) {
-        bound = pending_max<G, PAIR>(s, rot, t, s0);
-        const int eu = protect_update(bound, tt, xnb);
+      const bool need = !(nb <= 0x1p1020);
+      if (__any_sync(0xffffffffu, need)) {
+        double mx = range_max<G, PAIR>(s, rot, t, rlo, s0);
+        if (W > 1 && w > 0) {
+          Pub& pk = pub[blk];
+          if (t == 0) pk.kseg[team] = kseg;
+          __syncwarp();
+          if (lane == 0) pub_release(&pk.flag, 2 * tm.gen - 1);
+          while (ld_relaxed(&pk.cnt) != w) {
+          }
+          asm volatile("fence.acq_rel.cta;" ::: "memory");
+          for (int v = 0; v < w; ++v) mx = dmaxd(mx, tm.red2[v * 8 + team]);
+          __syncwarp();
+          if (lane == 0) pk.cnt = 0;
+        }
+        bound = mx;   // every column of the task (as one warp would)
+        eu = protect_update(bound, tt, xnb);
         if (eu < 0) {
           s.scale(eu);
           ex += eu;
@@ -476,35 +1052,54 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         aT[kk] = PAIR ? (comp ? (a * xi + b * xr) : (a * xr - b * xi)) : a * xr;
       }
       const double keep = s.y[PRV][1];   // solved straddling row: kept out of the update
-#pragma unroll
-      for (int q = 0; q < G - 1; ++q) {
-        const int g = blk - (CUR - q);     // group at position q (pending iff g >= 0)
-        if (g >= 0) {
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk) {
-            if (kk == 2 && !st) continue;
-            const int src0 = (kk < 2) ? g8 + 4 * kk : g8 - 4;
-            const double2 v = sm.ST[poff3(min(src0 + t, nt - 1)) + 8 * g + team];
-            dmma3(s.y[q][0], s.y[q][1], aS[kk], v.x);
-            dmma3(s.y[q][0], s.y[q][1], aT[kk], v.y);
-          }
-        }
-      }
+      dmma_block<G>(s, blk, blk, gmin, st, sm, nt, t, team, aS, aT);
       if (st && t == 3) s.y[PRV][1] = keep;
     }
+    ZZ_TR(blk * 8 + 3);
+    if (W > 1) {
+      // ---- publish the block: its rows at the segment's new scale, the scalings, the chain
+      // state (slot r of column `team` rescaled by lane r & 3: after the __syncwarp above) ----
+      if (eu < 0)
+        for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], eu);
+      Pub& pk = pub[blk];
+      if (t == 0) {
+        pk.kseg[team] = kseg;
+        pk.eu[team] = eu;
+        pk.ex[team] = ex;
+        pk.bound[team] = bound;
+      }
+      __syncwarp();
+      if (lane == 0) pub_release(&pk.flag, 2 * tm.gen);
+    }
+    ZZ_TR(blk * 8 + 4);
     s.rotate();
     ++rot;
+  }
+  // ---- the scalings of the blocks above this warp's range: one exponent per segment ----
+  if (W > 1) {
+    for (int k = lo - 1; k >= 0; --k) {
+      const Pub& pk = pub[k];
+      pub_wait(&pk.flag, 2 * tm.gen, lane);
+      const int k1 = pk.kseg[team], k2 = pk.eu[team];
+      if (k1 < 0) s.scale(k1);
+      if (k2 < 0) s.scale(k2);
+    }
+    if (!(lo == 0 && hi > 0)) ex = pub[0].ex[team];   // (block 0's publication was awaited above)
   }
   // ---- segment norms, exponent and the scaling decision of the next update (a5) ----
   double lm = 0.0, lh = 0.0;
 #pragma unroll
   for (int q = 0; q < G; ++q) {
+    const int g = (q - rot % G + G) % G;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
+      const int r = 8 * g + 2 * t + i;
       const double v = s.y[q][i];
       const double o = PAIR ? __shfl_xor_sync(0xffffffffu, v, 4) : 0.0;
-      lm = fmax(lm, fabs(v));
-      lh = fmax(lh, PAIR ? __dadd_rn(__dmul_rn(0.5, fabs(v)), __dmul_rn(0.5, fabs(o))) : __dmul_rn(0.5, fabs(v)));
+      if (r >= rlo && r < rhi) {
+        lm = fmax(lm, fabs(v));
+        lh = fmax(lh, PAIR ? __dadd_rn(__dmul_rn(0.5, fabs(v)), __dmul_rn(0.5, fabs(o))) : __dmul_rn(0.5, fabs(v)));
+      }
     }
   }
   lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, 1));
@@ -512,12 +1107,26 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   lh = fmax(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
   lh = fmax(lh, __shfl_xor_sync(0xffffffffu, lh, 2));
   if (PAIR) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, 4));
-  const int ep = (valid && !tip) ? P.e_pend[c] : 0;
+  if (W > 1) {   // over the team (exact, order-independent)
+    if (t == 0) {
+      tm.red1[(w * 8 + team) * 2] = lm;
+      tm.red1[(w * 8 + team) * 2 + 1] = lh;
+    }
+    team_sync(tm);
+    lm = 0.0;
+    lh = 0.0;
+    for (int v = 0; v < W; ++v) {
+      lm = fmax(lm, tm.red1[(v * 8 + team) * 2]);
+      lh = fmax(lh, tm.red1[(v * 8 + team) * 2 + 1]);
+    }
+  }
+  const bool w0 = (w == 0);   // the team's warp 0 writes the per-column state
+  ZZ_TR(140 + w);
   const int es = ep + ex;
   int sx = 0;
   if (valid) {
     const long long so = (long long)p.I * p.n_sel + c;
-    if (t == 0) {
+    if (t == 0 && w0) {
       P.e_seg[so] = es;
       P.nrm_seg[so] = lm;
       P.nrmh_seg[so] = lh;
@@ -555,7 +1164,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       const double yh = scale2k(nyv, g0 - e_p);
       const int ef = g0 + protect_update(yh, tau, xh);
       sx = ef - es;
-      if (t == 0) {
+      if (t == 0 && w0) {
         P.sY[c] = ef - e_p;
         P.e_pend[c] = ef;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
@@ -568,7 +1177,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       // active at that step (stale entries)
 #pragma unroll
       for (int k = 0; k < kMaxGroup - 1; ++k) {
-        if (k < p.n_prev) {
+        if (k < p.n_prev && w0) {
           const bool act = c0 >= p.prev_cs[k];
           const int ek = act ? P.e_grp[(long long)k * p.n_sel + c] : 0;
           if (!act || ef != ek) {
@@ -601,7 +1210,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       const double tau = __dadd_rn(__dmul_rn(beta, P.cS[p.I]), __dmul_rn(ab, P.cT[p.I]));
       const int en = g0 + protect_update(yh, tau, xh);
       sx = en - es;
-      if (t == 0) {
+      if (t == 0 && w0) {
         // lookahead: a shift taken on the recorded bound rather than the measured maximum may
         // over-scale; flag it, and the call is recomputed without lookahead (zz_api.cu)
         if (p.use_bound && en < g0) atomicOr(&P.status[6], 1);
@@ -628,7 +1237,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
       const int r = 8 * g + 2 * t + i;
       const double v = s.y[q][i];
       const double o = PAIR ? __shfl_xor_sync(0xffffffffu, v, 4) : 0.0;
-      if (valid && r < nt) {
+      if (valid && r >= rlo && r < rhi) {
         xo[r] = v;
         if (p.do_update) {
           const double xs = (sx >= -1022) ? v * fx : scale2_slow3(v, sx);
@@ -641,7 +1250,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     }
   }
   // zero rows nt .. nks*BK-1 (the K padding of the last chunk)
-  if (valid && p.do_update) {
+  if (valid && p.do_update && w0) {
     for (int r = nt + t; r < p.nks * kBK; r += 4) {
       const long long off = (long long)(r / kBK) * (kBN * kBK) + (long long)((r % kBK) >> 2) * (kBN * 4) + (r & 3);
       Wc[off] = 0.0;
@@ -650,6 +1259,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   }
   // W is read next by bulk copies (the async proxy): order the generic writes before them
   asm volatile("fence.proxy.async.global;" ::: "memory");
+  ZZ_TR(160 + w);
 }
 
 template <int G>
@@ -657,8 +1267,27 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   constexpr int kW3 = W3<G>::n;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int nt = p.nt;
-  Sm3 sm = carve3(smraw, nt);
+  ZZ_TR0();
+  const int W = p.team_w, nteams = kW3 / W;
+  const int nblk = (nt + 7) / 8;
+  const size_t tb = a16(team_bytes(W, nblk));
+  Sm3 sm = carve3(smraw, nt, nteams, tb, kW3);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tix = warp / W;
+  Team tm;
+  tm.W = W;
+  tm.w = warp % W;
+  tm.bar = 1 + tix;
+  tm.pub = reinterpret_cast<Pub*>(sm.teams + tb * tix);
+  const int nslot = (W == 1) ? 1 : nblk;
+  tm.pslab = sm.ptab + 576 * warp;
+  tm.red0 = reinterpret_cast<double*>(tm.pub + nslot);
+  tm.red1 = tm.red0 + 8 * W;
+  tm.red2 = tm.red1 + 16 * W;
+  for (int i = tm.w * 32 + lane; i < nslot; i += 32 * W) {
+    tm.pub[i].flag = 0;
+    tm.pub[i].cnt = 0;
+  }
   // ---- stage the diagonal tile: (S_ij, T_ij) for i <= j, (S_{j+1,j}, 0) below ----
   const int plen = nt * (nt + 3) / 2;
   // asynchronous 8-byte global->shared copies (cp.async): every element of the tile is in
@@ -682,7 +1311,6 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   for (int i = threadIdx.x; i < nt; i += blockDim.x) sm.fl[i] = p.P.row_flag[p.t0 + i];
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  const int nblk = (nt + 7) / 8;
   if (threadIdx.x <= nblk) {
     const int b = threadIdx.x;
     int v = 8 * b;
@@ -731,15 +1359,32 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
       mt = fmax(mt, __shfl_xor_sync(0xffffffffu, mt, o));
     }
     if (lane == 0) sm.tau[b] = make_double2(ms, mt);
+    // ||S_bb||_inf, ||T_bb||_inf of the block's diagonal sub-block (gsolve_block's condition
+    // check): lane i < e0 - s0 sums row s0 + i over the block's columns
+    double bs_ = 0.0, bt_ = 0.0;
+    if (lane < e0 - s0) {
+      const int i = s0 + lane;
+      for (int l = max(s0, i - 1); l < e0; ++l) {
+        const double2 v = sm.ST[poff3(l) + i];
+        bs_ += fabs(v.x);
+        bt_ += fabs(v.y);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      bs_ = fmax(bs_, __shfl_xor_sync(0xffffffffu, bs_, o));
+      bt_ = fmax(bt_, __shfl_xor_sync(0xffffffffu, bt_, o));
+    }
+    if (lane == 0) sm.bn[b] = make_double2(bs_, bt_);
   }
   __syncthreads();
-  // ---- tasks: 4 complex pairs or 8 real columns per warp ----
+  // ---- tasks (4 complex pairs or 8 real columns), one per team of W warps ----
   const int npt = (p.n_pair + p.cpt / 2 - 1) / (p.cpt / 2), nrt = (p.n_real + p.cpt - 1) / p.cpt;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two
   // (measured: contiguous per-CTA task ranges were slower, pair tasks being heavier)
-  for (int task = warp * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * kW3) {
-    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, sm.slab + warp * 72, sm.pslab + warp * 576);
-    else solve_task<G, false>(p, sm, nblk, task - npt, lane, sm.slab + warp * 72, sm.pslab + warp * 576);
+  for (int task = tix * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * nteams) {
+    tm.gen = task + 1;
+    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, tm);
+    else solve_task<G, false>(p, sm, nblk, task - npt, lane, tm);
   }
 }
 
@@ -747,7 +1392,10 @@ int g_sms3 = 0;
 
 }  // namespace
 
-size_t diag3_smem_bytes(int nt) { return smem3(nt); }
+size_t diag3_smem_bytes(int nt) {
+  const int nblk = (nt + 7) / 8;
+  return smem3(nt, 12, a16(team_bytes(1, nblk)), 12);
+}
 
 cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
   Diag2Params p = pin;
@@ -762,20 +1410,43 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
   const int tasks = (p.n_pair + 3) / 4 + (p.n_real + 7) / 8;
   if (tasks == 0) return cudaSuccess;
   if (p.nt > kDiag2MaxNT) return cudaErrorInvalidValue;
-  const size_t smem = smem3(p.nt);
+  const int nblk = (p.nt + 7) / 8;
+  const bool small = p.nt <= 64;
+  const int nw = small ? W3<8>::n : W3<16>::n;
+  // team size W (a divisor of the CTA's warps): as many warps per task as keep every task in
+  // one wave over the SMs -- the chain of a task then runs on W warps (results do not
+  // depend on W, see solve_task); limited by the shared memory of the teams
+  // Automatic: one warp per task.  Measured (C2, tools/time_team.py): teams are slower --
+  // the hand-off of a block between warps costs about as much as the DMMA updates it spreads
+  // (DESIGN.md s.6 "Teams"); zz_set_diag_team(W) selects them explicitly.
+  int W = 1;
+  if (p.team_w > 0) {
+    W = p.team_w;
+    if (nw % W || smem3(p.nt, nw / W, a16(team_bytes(W, nblk)), nw) > 227 * 1024) W = 1;
+  } else if (p.team_w < 0 && !p.pack) {
+    const int cand[5] = {small ? 16 : 12, small ? 8 : 6, 4, small ? 2 : 3, 1};
+    for (int i = 0; i < 5; ++i) {
+      const int Wc = cand[i];
+      if ((long long)tasks * Wc > (long long)g_sms3 * nw) continue;
+      if (smem3(p.nt, nw / Wc, a16(team_bytes(Wc, nblk)), nw) > 227 * 1024) continue;
+      W = Wc;
+      break;
+    }
+  }
+  p.team_w = W;
+  const int per_cta = nw / W;   // tasks per CTA at a time
+  const size_t smem = smem3(p.nt, per_cta, a16(team_bytes(W, nblk)), nw);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e;
-  // pack: as few CTAs as the tasks need (one task per warp), leaving the other SMs to a
+  // pack: as few CTAs as the tasks need (one task per team), leaving the other SMs to a
   // concurrent update (lookahead); otherwise one task per CTA first (lowest latency alone)
-  if (p.nt <= 64) {
-    constexpr int nw = W3<8>::n;
-    const int grid = p.pack ? std::min(g_sms3, (tasks + nw - 1) / nw) : (tasks < g_sms3 ? tasks : g_sms3);
-    e = cudaFuncSetAttribute(k_diag3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = p.pack ? std::min(g_sms3, (tasks + per_cta - 1) / per_cta) : (tasks < g_sms3 ? tasks : g_sms3);
+  if (small) {
+    e = cudaFuncSetAttribute(k_diag3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     k_diag3<8><<<grid, nw * 32, smem, st>>>(p);
   } else {
-    constexpr int nw = W3<16>::n;
-    const int grid = p.pack ? std::min(g_sms3, (tasks + nw - 1) / nw) : (tasks < g_sms3 ? tasks : g_sms3);
-    e = cudaFuncSetAttribute(k_diag3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_diag3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     k_diag3<16><<<grid, nw * 32, smem, st>>>(p);
   }
@@ -783,3 +1454,9 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
 }
 
 }  // namespace zz
+
+#ifdef ZZ_VARIANT_TRACE
+extern "C" int zz_trace_get(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, zz::g_trace, sizeof(long long) * 256);
+}
+#endif

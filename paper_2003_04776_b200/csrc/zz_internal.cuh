@@ -173,6 +173,7 @@ struct Diag2Params {
   // group's last step (use_bound) instead of the measured maximum; the last step records it
   int use_bound, record_bound;
   int pack;                // launch as few CTAs as the tasks need (lookahead)
+  int team_w;              // warps per task (0: chosen by launch_diag3; results do not depend on it)
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)

@@ -764,3 +764,29 @@ def test_graph_replay_bitwise(zz):
                 assert np.array_equal(Xs1, Xs0) and np.array_equal(es1, es0)
     finally:
         zz.set_graphs(True)
+
+
+@pytest.mark.parametrize("name,mb,teams", [("C2", 128, (1, 3, 4, 6, 12)), ("C2", 64, (1, 2, 4, 8, 16)),
+                                           ("C1", 32, (1, 2, 4, 16)), ("stress1000", 128, (1, 4, 12))])
+def test_diag_team_bitwise(zz, name, mb, teams):
+    """Teams of warps per diagonal-solve task (include/zz.h zz_set_diag_team): every team
+    size gives the bits of one warp per task (the same instructions on the same operands per
+    column), with and without a selection and on a stress pencil whose scalings trigger; and
+    the automatic choice is in parity with the oracle."""
+    if name == "stress1000":
+        S, T = _stress(1000, 1)
+    else:
+        S, T, _ = gen.config(name, seed=5)
+    sel = (np.random.default_rng(2).random(S.shape[0]) < 0.2).astype(np.int32)
+    try:
+        for select in (None, sel):
+            zz.set_diag_team(1)
+            X0, e0, info0 = solve(zz, S, T, mb=mb, select=select)
+            for w in teams + (0, -1):
+                zz.set_diag_team(w)
+                X1, e1, _ = solve(zz, S, T, mb=mb, select=select)
+                assert np.array_equal(X1, X0) and np.array_equal(e1, e0), (name, mb, w)
+            if name != "stress1000":
+                check_against_oracle(S, T, X0, e0, select=select, info=info0)
+    finally:
+        zz.set_diag_team(0)
