@@ -118,7 +118,7 @@ struct Team {
 };
 
 #ifdef ZZ_VARIANT_TRACE
-__device__ long long g_trace[256];
+__device__ long long g_trace[512];
 #define ZZ_TR(i) do { if (blockIdx.x == 0 && tm.gen == 1 && lane == 0) g_trace[(i)] = clock64(); } while (0)
 #define ZZ_TR0() do { if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[180] = clock64(); } while (0)
 #else
@@ -314,7 +314,7 @@ struct GRows {
 // pair -- inv row 0 at [J][0..3], row 1 at [J+1][0..3] (complex).  A rolled loop (compact code:
 // the diagonal solve is bound by instruction fetch when its code is unrolled).
 template <bool PAIR>
-__device__ __noinline__ void gpiv_block(const Sm3& sm, int r0, int q0, int qe, double a, double b, double beta,
+__device__ __forceinline__ void gpiv_block(const Sm3& sm, int r0, int q0, int qe, double a, double b, double beta,
                                         double ab, int u, int col, double* ptab) {
   const int nl = PAIR ? 8 : 4;
 #pragma unroll 1
@@ -590,15 +590,19 @@ template <int G>
 __device__ __forceinline__ void dmma_block(Seg<G>& s, int top, int k, int gmin, bool st, const Sm3& sm, int nt,
                                            int t, int team, const double (&aS)[3], const double (&aT)[3]) {
   const int g8 = 8 * k;
+  // source chunk outermost: consecutive DMMAs belong to different groups (independent
+  // accumulators), so they issue back to back instead of waiting on each other; per group the
+  // order of the products (kk = 0, 1, 2; S then T) is unchanged
 #pragma unroll
-  for (int q = 0; q < G; ++q) {
-    const int g = top - (G - 1 - q);
-    if (g >= gmin && g < k) {
+  for (int kk = 0; kk < 3; ++kk) {
+    if (kk == 2 && !st) continue;
+    const int src0 = (kk < 2) ? g8 + 4 * kk : g8 - 4;
+    const double2* col = sm.ST + poff3(min(src0 + t, nt - 1)) + team;
 #pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        if (kk == 2 && !st) continue;
-        const int src0 = (kk < 2) ? g8 + 4 * kk : g8 - 4;
-        const double2 v = sm.ST[poff3(min(src0 + t, nt - 1)) + 8 * g + team];
+    for (int q = 0; q < G; ++q) {
+      const int g = top - (G - 1 - q);
+      if (g >= gmin && g < k) {
+        const double2 v = col[8 * g];
         dmma3(s.y[q][0], s.y[q][1], aS[kk], v.x);
         dmma3(s.y[q][0], s.y[q][1], aT[kk], v.y);
       }
@@ -626,11 +630,182 @@ __device__ __forceinline__ void pub_frags(const double* x, const Sm3& sm, int k,
   }
 }
 
+// The protected substitution of one block (P:142-146 with ProtectDivision / ProtectUpdate,
+// P:175-200): the rows of the block in the warp's slab, solved 1x1 / 2x2 block by 1x1 / 2x2
+// block bottom-up with in-block updates against the running bound.  Out of line: the block-local
+// inverse handles almost every block, and the diagonal solve is bound by instruction fetch.
+struct SlowSt { double bound, xnb; int ex, kseg; };
+
+template <bool PAIR>
+__device__ __forceinline__ SlowSt slow_block(const Sm3& sm, double* wslab, double* pslab, int g8, int q0, int s0,
+                                          int e0, double a, double b, double beta, double ab, bool tip, int tipr,
+                                          int team, int t, int comp, SlowSt st) {
+  double bound = st.bound, xnb = st.xnb;
+  int ex = st.ex, kseg = st.kseg;
+  // pivots of the block's 1x1 rows, off the dependency chain: lane t prepares slots t,
+  // t+4, t+8 of its column -- the perturbed pivot d (R8), its reciprocal (real) or Smith's
+  // ratio and denominator (pair), and the ProtectDivision threshold (|w| <= thr: no scaling)
+  for (int q = t; q < 9; q += 4) {
+    const int j = g8 - 1 + q;
+    if (q < q0 || j >= e0 || sm.fl[j] != kRow1x1) continue;
+    const double2 dd = sm.ST[poff3(j) + j];
+    cpx d = mkc(__fma_rn(-a, dd.y, __dmul_rn(beta, dd.x)), __dmul_rn(-b, dd.y));
+    const double smin =
+        dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, fabs(dd.x)), __dmul_rn(ab, fabs(dd.y)))), kSmlnum);
+    if (n1(d) < smin) d = mkc(smin, 0.0);
+    double* pd = pslab + (q * 8 + team) * 8;
+    pd[0] = d.re;
+    pd[1] = d.im;
+    if (!PAIR) {
+      const double td = fabs(d.re);
+      pd[2] = __drcp_rn(d.re);
+      pd[3] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
+    } else {
+      const double td = __dmul_rn(0.5, dmind(1.0, nmax(d)));
+      const bool re_dom = fabs(d.re) >= fabs(d.im);
+      const double sr = re_dom ? __ddiv_rn(d.im, d.re) : __ddiv_rn(d.re, d.im);
+      const double den = re_dom ? __dadd_rn(d.re, __dmul_rn(d.im, sr)) : __dadd_rn(d.im, __dmul_rn(d.re, sr));
+      pd[2] = sr;
+      pd[3] = den;
+      pd[4] = __drcp_rn(den);
+      pd[5] = re_dom ? 1.0 : 0.0;
+      pd[6] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
+    }
+  }
+  __syncwarp();
+  int j = e0 - 1;
+  while (j >= s0) {
+    const int q = j - (g8 - 1);
+    const bool two = sm.fl[j] == kRowBot2;
+    const int qs = two ? q - 1 : q;
+    const int pt = PAIR ? (team & ~1) : team;     // (Re, Im) entries of the pair
+    int k = 0;
+    cpx xt, xb;
+    {
+      cpx wb = mkc(wslab[q * 8 + pt], PAIR ? wslab[q * 8 + pt + 1] : 0.0);
+      if (two) {
+        cpx wt = mkc(wslab[(q - 1) * 8 + pt], PAIR ? wslab[(q - 1) * 8 + pt + 1] : 0.0);
+        const double2 d11 = sm.ST[poff3(j - 1) + j - 1], d21 = sm.ST[poff3(j - 1) + j];
+        const double2 d12 = sm.ST[poff3(j) + j - 1], d22 = sm.ST[poff3(j) + j];
+        solve2x2<PAIR>(wt, wb, d11.x, d21.x, d12.x, d22.x, d11.y, d12.y, d22.y, a, b, beta, ab, k);
+        if (PAIR && tip && tipr == j) {
+          // tip of a complex pair (reading R10): rows (r-1, r) of the eigenvalue block
+          const double pp = __dmul_rn(beta, d21.x);
+          const cpx qq = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
+          if (fabs(pp) >= n1(qq)) {
+            wb = mkc(1.0, 0.0);
+            wt = mkc(__ddiv_rn(-qq.re, pp), __ddiv_rn(-qq.im, pp));
+          } else {
+            wt = mkc(1.0, 0.0);
+            const cpx z = cdivx(mkc(pp, 0.0), qq);
+            wb = mkc(-z.re, -z.im);
+          }
+          k = 0;
+        }
+        xt = wt;
+        xb = wb;
+      } else {
+        // (beta S_jj - alpha T_jj) x = w with the prepared pivot: q = w r corrected once by
+        // the residual (the quotient of __ddiv_rn); scaling only past the threshold
+        const double* pd = pslab + (q * 8 + team) * 8;
+        const cpx d = mkc(pd[0], pd[1]);
+        if (!PAIR) {
+          const double r = pd[2];
+          if (fabs(wb.re) <= pd[3]) {
+            const double x0 = wb.re * r;
+            xb = mkc(fma(r, fma(-d.re, x0, wb.re), x0), 0.0);
+          } else {
+            xb = pdiv3<false>(wb, d, k);
+          }
+        } else {
+          if (nmax(wb) <= pd[6]) {
+            const double sr = pd[2], den = pd[3], rd = pd[4];
+            const double n1v = (pd[5] != 0.0) ? __dadd_rn(wb.re, __dmul_rn(wb.im, sr))
+                                              : __dadd_rn(__dmul_rn(wb.re, sr), wb.im);
+            const double n2v = (pd[5] != 0.0) ? __dsub_rn(wb.im, __dmul_rn(wb.re, sr))
+                                              : __dsub_rn(__dmul_rn(wb.im, sr), wb.re);
+            const double y1 = n1v * rd, y2 = n2v * rd;
+            xb = mkc(fma(rd, fma(-den, y1, n1v), y1), fma(rd, fma(-den, y2, n2v), y2));
+          } else {
+            xb = pdiv3<true>(wb, d, k);
+          }
+        }
+        if (!PAIR && tip && tipr == j) { xb = mkc(1.0, 0.0); k = 0; }
+        xt = xb;
+      }
+    }
+    // scalars follow the solve's scaling at once; the stored values once (below)
+    if (k < 0) {
+      bound = scale2k(bound, k);
+      xnb = scale2k(xnb, k);
+    }
+    double xn = two ? dmaxd(nmax(xt), nmax(xb)) : nmax(xb);
+    int eu = 0;
+    double tt = 0.0;
+    const bool upd = qs > q0;
+    if (upd) {
+      // in-block update of the block rows above (ProtectUpdate) against a running
+      // upper bound of the pending rows; lane-local (every lane holds the same values)
+      const double2 cmv = sm.cm[j];
+      tt = __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y));
+      double nb = fma(tt, xn, bound);
+      if (!(nb <= 0x1p1020)) {
+        eu = protect_update(bound, tt, xn);
+        nb = __dadd_rn(scale2k(bound, eu), __dmul_rn(tt, scale2k(xn, eu)));
+      }
+      bound = nb;
+    }
+    if (k + eu < 0) {
+      // the whole segment by 2^(k+eu): the block's rows in the slab now, the rows in
+      // registers once after the row loop (kseg) -- s.y is then not modified inside the
+      // loop, so it keeps its registers (no copies around the loop; powers of two)
+      const int kk = k + eu;
+      kseg += kk;
+      // slot r of the slab is always written by lane r & 3 of its column (here and in the
+      // update below), so no warp barrier is needed in this column-divergent branch
+      for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], kk);
+      ex += kk;
+      if (eu < 0) {
+        xnb = scale2k(xnb, eu);
+        xn = scale2k(xn, eu);
+        xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
+        xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
+      }
+    }
+    xnb = dmaxd(xnb, xn);
+    if (upd) {
+      // sources in ascending row order, as the oracle's O6; each lane updates the rows of
+      // its column (4 lanes split the rows)
+#pragma unroll
+      for (int sidx = 0; sidx < 2; ++sidx) {
+        if (sidx == 0 && !two) continue;
+        const cpx x = sidx ? xb : xt;
+        const double xo = PAIR ? (comp ? x.im : x.re) : x.re;
+        const double ur = beta * xo;
+        const double wr = PAIR ? (comp ? (a * x.im + b * x.re) : (a * x.re - b * x.im)) : a * x.re;
+        const double2* col = sm.ST + poff3(sidx ? j : j - 1) + (g8 - 1);
+        for (int r = q0 + ((t - q0) & 3); r < qs; r += 4) {
+          const double2 v = col[r];
+          wslab[r * 8 + team] = fma(v.y, wr, fma(-v.x, ur, wslab[r * 8 + team]));
+        }
+      }
+    }
+    // the solution into the slab (own component; slot r by lane r & 3)
+    if (t == (q & 3)) wslab[q * 8 + team] = PAIR ? (comp ? xb.im : xb.re) : xb.re;
+    if (two && t == ((q - 1) & 3)) wslab[(q - 1) * 8 + team] = PAIR ? (comp ? xt.im : xt.re) : xt.re;
+    __syncwarp();
+    j = qs - 1 + (g8 - 1);
+  }
+  st.bound = bound; st.xnb = xnb; st.ex = ex; st.kseg = kseg;
+  return st;
+}
+
 // ------------------------------------------------------------------------------------
 // One task: 8 real columns (PAIR = false) or 4 complex pairs (PAIR = true) of tile I.
 // ------------------------------------------------------------------------------------
-template <int G, bool PAIR>
-__device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane, const Team& tm) {
+template <int G, bool PAIR, bool TEAMS>
+__device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane,
+                                        const Team& tm) {
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
@@ -666,7 +841,7 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   // (the same DMMA instructions on the same operands as the block's owner would issue), so
   // the arithmetic of a column does not depend on W.  Group lo-1 is kept as well when it
   // holds the top row of a 2x2 block that straddles into block lo. ----
-  const int W = tm.W, w = tm.w;
+  const int W = TEAMS ? tm.W : 1, w = TEAMS ? tm.w : 0;   // (one warp: the team code compiles away)
   const int lo = (w * nblk) / W, hi = ((w + 1) * nblk) / W;
   const int rlo = sm.bs[lo], rhi = sm.bs[hi];
   const int gmin = (lo > 0 && rlo < 8 * lo) ? lo - 1 : lo;
@@ -775,10 +950,13 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     const int u = PAIR ? comp * 4 + t : t;
     if (blk != pre_blk)
       gpiv_block<PAIR>(sm, g8 - 1, q0, e0 - (g8 - 1), a * gsc, b * gsc, beta * gsc, ab * gsc, u, PAIR ? (team & ~1) : team, pslab);
+    ZZ_TR(256 + blk * 8 + 0);
     GRows gpre;
     gprep_block<PAIR>(sm, g8, q0, e0 - (g8 - 1), nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u,
                       PAIR ? (team & ~1) : team, pslab, gpre);
+    ZZ_TR(256 + blk * 8 + 1);
     bool okc = gapply_block<PAIR>(gpre, wslab, q0, e0 - (g8 - 1), dn, gsc, team, u, xfr, xfi);
+    ZZ_TR(256 + blk * 8 + 2);
 #ifndef ZZ_VARIANT_NOTIP
     okc = okc && !(tip && tipr >= s0 && tipr < e0);
 #endif
@@ -797,159 +975,11 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
     if (__any_sync(0xffffffffu, !okc)) {
     const double bound0 = bound;
     const int ex0 = ex;
-    // pivots of the block's 1x1 rows, off the dependency chain: lane t prepares slots t,
-    // t+4, t+8 of its column -- the perturbed pivot d (R8), its reciprocal (real) or Smith's
-    // ratio and denominator (pair), and the ProtectDivision threshold (|w| <= thr: no scaling)
-    for (int q = t; q < 9; q += 4) {
-      const int j = g8 - 1 + q;
-      if (q < q0 || j >= e0 || sm.fl[j] != kRow1x1) continue;
-      const double2 dd = sm.ST[poff3(j) + j];
-      cpx d = mkc(__fma_rn(-a, dd.y, __dmul_rn(beta, dd.x)), __dmul_rn(-b, dd.y));
-      const double smin =
-          dmaxd(__dmul_rn(kU, __dadd_rn(__dmul_rn(beta, fabs(dd.x)), __dmul_rn(ab, fabs(dd.y)))), kSmlnum);
-      if (n1(d) < smin) d = mkc(smin, 0.0);
-      double* pd = pslab + (q * 8 + team) * 8;
-      pd[0] = d.re;
-      pd[1] = d.im;
-      if (!PAIR) {
-        const double td = fabs(d.re);
-        pd[2] = __drcp_rn(d.re);
-        pd[3] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
-      } else {
-        const double td = __dmul_rn(0.5, dmind(1.0, nmax(d)));
-        const bool re_dom = fabs(d.re) >= fabs(d.im);
-        const double sr = re_dom ? __ddiv_rn(d.im, d.re) : __ddiv_rn(d.re, d.im);
-        const double den = re_dom ? __dadd_rn(d.re, __dmul_rn(d.im, sr)) : __dadd_rn(d.im, __dmul_rn(d.re, sr));
-        pd[2] = sr;
-        pd[3] = den;
-        pd[4] = __drcp_rn(den);
-        pd[5] = re_dom ? 1.0 : 0.0;
-        pd[6] = (td >= 1.0) ? INFINITY : __dmul_rn(td, kOmega);
-      }
-    }
-    __syncwarp();
-    int j = e0 - 1;
-    while (j >= s0) {
-      const int q = j - (g8 - 1);
-      const bool two = sm.fl[j] == kRowBot2;
-      const int qs = two ? q - 1 : q;
-      const int pt = PAIR ? (team & ~1) : team;     // (Re, Im) entries of the pair
-      int k = 0;
-      cpx xt, xb;
-      {
-        cpx wb = mkc(wslab[q * 8 + pt], PAIR ? wslab[q * 8 + pt + 1] : 0.0);
-        if (two) {
-          cpx wt = mkc(wslab[(q - 1) * 8 + pt], PAIR ? wslab[(q - 1) * 8 + pt + 1] : 0.0);
-          const double2 d11 = sm.ST[poff3(j - 1) + j - 1], d21 = sm.ST[poff3(j - 1) + j];
-          const double2 d12 = sm.ST[poff3(j) + j - 1], d22 = sm.ST[poff3(j) + j];
-          solve2x2<PAIR>(wt, wb, d11.x, d21.x, d12.x, d22.x, d11.y, d12.y, d22.y, a, b, beta, ab, k);
-          if (PAIR && tip && tipr == j) {
-            // tip of a complex pair (reading R10): rows (r-1, r) of the eigenvalue block
-            const double pp = __dmul_rn(beta, d21.x);
-            const cpx qq = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
-            if (fabs(pp) >= n1(qq)) {
-              wb = mkc(1.0, 0.0);
-              wt = mkc(__ddiv_rn(-qq.re, pp), __ddiv_rn(-qq.im, pp));
-            } else {
-              wt = mkc(1.0, 0.0);
-              const cpx z = cdivx(mkc(pp, 0.0), qq);
-              wb = mkc(-z.re, -z.im);
-            }
-            k = 0;
-          }
-          xt = wt;
-          xb = wb;
-        } else {
-          // (beta S_jj - alpha T_jj) x = w with the prepared pivot: q = w r corrected once by
-          // the residual (the quotient of __ddiv_rn); scaling only past the threshold
-          const double* pd = pslab + (q * 8 + team) * 8;
-          const cpx d = mkc(pd[0], pd[1]);
-          if (!PAIR) {
-            const double r = pd[2];
-            if (fabs(wb.re) <= pd[3]) {
-              const double x0 = wb.re * r;
-              xb = mkc(fma(r, fma(-d.re, x0, wb.re), x0), 0.0);
-            } else {
-              xb = pdiv3<false>(wb, d, k);
-            }
-          } else {
-            if (nmax(wb) <= pd[6]) {
-              const double sr = pd[2], den = pd[3], rd = pd[4];
-              const double n1v = (pd[5] != 0.0) ? __dadd_rn(wb.re, __dmul_rn(wb.im, sr))
-                                                : __dadd_rn(__dmul_rn(wb.re, sr), wb.im);
-              const double n2v = (pd[5] != 0.0) ? __dsub_rn(wb.im, __dmul_rn(wb.re, sr))
-                                                : __dsub_rn(__dmul_rn(wb.im, sr), wb.re);
-              const double y1 = n1v * rd, y2 = n2v * rd;
-              xb = mkc(fma(rd, fma(-den, y1, n1v), y1), fma(rd, fma(-den, y2, n2v), y2));
-            } else {
-              xb = pdiv3<true>(wb, d, k);
-            }
-          }
-          if (!PAIR && tip && tipr == j) { xb = mkc(1.0, 0.0); k = 0; }
-          xt = xb;
-        }
-      }
-      // scalars follow the solve's scaling at once; the stored values once (below)
-      if (k < 0) {
-        bound = scale2k(bound, k);
-        xnb = scale2k(xnb, k);
-      }
-      double xn = two ? dmaxd(nmax(xt), nmax(xb)) : nmax(xb);
-      int eu = 0;
-      double tt = 0.0;
-      const bool upd = qs > q0;
-      if (upd) {
-        // in-block update of the block rows above (ProtectUpdate) against a running
-        // upper bound of the pending rows; lane-local (every lane holds the same values)
-        const double2 cmv = sm.cm[j];
-        tt = __dadd_rn(__dmul_rn(beta, cmv.x), __dmul_rn(ab, cmv.y));
-        double nb = fma(tt, xn, bound);
-        if (!(nb <= 0x1p1020)) {
-          eu = protect_update(bound, tt, xn);
-          nb = __dadd_rn(scale2k(bound, eu), __dmul_rn(tt, scale2k(xn, eu)));
-        }
-        bound = nb;
-      }
-      if (k + eu < 0) {
-        // the whole segment by 2^(k+eu): the block's rows in the slab now, the rows in
-        // registers once after the row loop (kseg) -- s.y is then not modified inside the
-        // loop, so it keeps its registers (no copies around the loop; powers of two)
-        const int kk = k + eu;
-        kseg += kk;
-        // slot r of the slab is always written by lane r & 3 of its column (here and in the
-        // update below), so no warp barrier is needed in this column-divergent branch
-        for (int r = t; r < 9; r += 4) wslab[r * 8 + team] = scale2k(wslab[r * 8 + team], kk);
-        ex += kk;
-        if (eu < 0) {
-          xnb = scale2k(xnb, eu);
-          xn = scale2k(xn, eu);
-          xt = mkc(scale2k(xt.re, eu), scale2k(xt.im, eu));
-          xb = mkc(scale2k(xb.re, eu), scale2k(xb.im, eu));
-        }
-      }
-      xnb = dmaxd(xnb, xn);
-      if (upd) {
-        // sources in ascending row order, as the oracle's O6; each lane updates the rows of
-        // its column (4 lanes split the rows)
-#pragma unroll
-        for (int sidx = 0; sidx < 2; ++sidx) {
-          if (sidx == 0 && !two) continue;
-          const cpx x = sidx ? xb : xt;
-          const double xo = PAIR ? (comp ? x.im : x.re) : x.re;
-          const double ur = beta * xo;
-          const double wr = PAIR ? (comp ? (a * x.im + b * x.re) : (a * x.re - b * x.im)) : a * x.re;
-          const double2* col = sm.ST + poff3(sidx ? j : j - 1) + (g8 - 1);
-          for (int r = q0 + ((t - q0) & 3); r < qs; r += 4) {
-            const double2 v = col[r];
-            wslab[r * 8 + team] = fma(v.y, wr, fma(-v.x, ur, wslab[r * 8 + team]));
-          }
-        }
-      }
-      // the solution into the slab (own component; slot r by lane r & 3)
-      if (t == (q & 3)) wslab[q * 8 + team] = PAIR ? (comp ? xb.im : xb.re) : xb.re;
-      if (two && t == ((q - 1) & 3)) wslab[(q - 1) * 8 + team] = PAIR ? (comp ? xt.im : xt.re) : xt.re;
-      __syncwarp();
-      j = qs - 1 + (g8 - 1);
+    {
+      SlowSt ss;
+      ss.bound = bound; ss.xnb = xnb; ss.ex = ex; ss.kseg = kseg;
+      ss = slow_block<PAIR>(sm, wslab, pslab, g8, q0, s0, e0, a, b, beta, ab, tip, tipr, team, t, comp, ss);
+      bound = ss.bound; xnb = ss.xnb; ex = ss.ex; kseg = ss.kseg;
     }
     if (okc) {   // the substitution ran for other columns of the warp: keep the fast result
       bound = bound0;
@@ -1052,7 +1082,9 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
         aT[kk] = PAIR ? (comp ? (a * xi + b * xr) : (a * xr - b * xi)) : a * xr;
       }
       const double keep = s.y[PRV][1];   // solved straddling row: kept out of the update
+      ZZ_TR(256 + blk * 8 + 3);
       dmma_block<G>(s, blk, blk, gmin, st, sm, nt, t, team, aS, aT);
+      ZZ_TR(256 + blk * 8 + 4);
       if (st && t == 3) s.y[PRV][1] = keep;
     }
     ZZ_TR(blk * 8 + 3);
@@ -1262,13 +1294,13 @@ __device__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int ta
   ZZ_TR(160 + w);
 }
 
-template <int G>
+template <int G, bool TEAMS>
 __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   constexpr int kW3 = W3<G>::n;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int nt = p.nt;
   ZZ_TR0();
-  const int W = p.team_w, nteams = kW3 / W;
+  const int W = TEAMS ? p.team_w : 1, nteams = kW3 / W;
   const int nblk = (nt + 7) / 8;
   const size_t tb = a16(team_bytes(W, nblk));
   Sm3 sm = carve3(smraw, nt, nteams, tb, kW3);
@@ -1383,8 +1415,8 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   // (measured: contiguous per-CTA task ranges were slower, pair tasks being heavier)
   for (int task = tix * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * nteams) {
     tm.gen = task + 1;
-    if (task < npt) solve_task<G, true>(p, sm, nblk, task, lane, tm);
-    else solve_task<G, false>(p, sm, nblk, task - npt, lane, tm);
+    if (task < npt) solve_task<G, true, TEAMS>(p, sm, nblk, task, lane, tm);
+    else solve_task<G, false, TEAMS>(p, sm, nblk, task - npt, lane, tm);
   }
 }
 
@@ -1441,15 +1473,20 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
   // pack: as few CTAs as the tasks need (one task per team), leaving the other SMs to a
   // concurrent update (lookahead); otherwise one task per CTA first (lowest latency alone)
   const int grid = p.pack ? std::min(g_sms3, (tasks + per_cta - 1) / per_cta) : (tasks < g_sms3 ? tasks : g_sms3);
+#define ZZ_LAUNCH3(GG, TT)                                                                           \
+  do {                                                                                              \
+    e = cudaFuncSetAttribute(k_diag3<GG, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
+    if (e != cudaSuccess) return e;                                                                 \
+    k_diag3<GG, TT><<<grid, nw * 32, smem, st>>>(p);                                                \
+  } while (0)
   if (small) {
-    e = cudaFuncSetAttribute(k_diag3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    k_diag3<8><<<grid, nw * 32, smem, st>>>(p);
+    if (W > 1) ZZ_LAUNCH3(8, true);
+    else ZZ_LAUNCH3(8, false);
   } else {
-    e = cudaFuncSetAttribute(k_diag3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    k_diag3<16><<<grid, nw * 32, smem, st>>>(p);
+    if (W > 1) ZZ_LAUNCH3(16, true);
+    else ZZ_LAUNCH3(16, false);
   }
+#undef ZZ_LAUNCH3
   return cudaGetLastError();
 }
 
@@ -1457,6 +1494,6 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
 
 #ifdef ZZ_VARIANT_TRACE
 extern "C" int zz_trace_get(long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, zz::g_trace, sizeof(long long) * 256);
+  return (int)cudaMemcpyFromSymbol(out, zz::g_trace, sizeof(long long) * 512);
 }
 #endif

@@ -16,7 +16,7 @@ for W in [int(w) for w in os.environ.get("TEAMS", "1,12").split(",")]:
     zz.set_diag_team(W)
     for _ in range(2):
         X, e = zz.tgevc(Sd, Td); torch.cuda.synchronize()
-    buf = (ctypes.c_longlong * 256)()
+    buf = (ctypes.c_longlong * 512)()
     lib.zz_trace_get(buf)
     tr = np.array(buf[:], dtype=np.int64)
     t0 = tr[180]
@@ -25,6 +25,6 @@ for W in [int(w) for w in os.environ.get("TEAMS", "1,12").split(",")]:
     print("  init  ", [rel(tr[200 + w]) for w in range(12)])
     print("  chain0", [rel(tr[220 + w]) for w in range(12)])
     for k in range(15, -1, -1):
-        print("  blk %2d" % k, [rel(tr[k * 8 + i]) for i in range(7)])
+        print("  blk %2d" % k, [rel(tr[k * 8 + i]) for i in range(7)], "fine", [rel(tr[256 + k * 8 + i]) for i in range(5)])
     print("  epi   ", [rel(tr[140 + w]) for w in range(12)])
     print("  end   ", [rel(tr[160 + w]) for w in range(12)])
