@@ -226,6 +226,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="plain stream launches instead of the captured wavefront (for ncu launch lists)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-blocks", type=int, default=192)
     ap.add_argument("--ref-blocks", type=int, default=192)
@@ -263,6 +265,8 @@ def main():
     m = cfg["m"]
     mb = args.mb
     zz.set_tile(mb)
+    if args.no_graphs:
+        zz.set_graphs(False)
 
     def barrier():
         if world > 1:

@@ -7,6 +7,7 @@ if os.environ.get("ZZLIB"):          # an alternative build of libzz.so (A/B)
     zz._SO = os.environ["ZZLIB"]
     zz.load(build_if_missing=False)
 zz.init(0)
+zz.set_graphs(False)   # ncu profiles individual launches
 if os.environ.get("TEAM"):
     zz.set_diag_team(int(os.environ["TEAM"]))
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"

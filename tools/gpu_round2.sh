@@ -18,14 +18,20 @@ if [ "${SWEEP:-1}" = "1" ]; then
 timeout 900 python tools/sweep.py > $OUT/${TAG}_sweep.json 2> $OUT/${TAG}_sweep.err; echo "sweep exit $?"
 fi
 if [ "${NCU:-1}" = "1" ]; then
-  CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-roofline"
+  CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-roofline --no-graphs"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/${TAG}_launches.csv $CMD > $OUT/${TAG}_ncu_launches.log 2>&1; echo "ncu launches exit $?"
-  CMD2="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-roofline"
+  CMD2="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-roofline --no-graphs"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
       -k regex:k_update_tILi1E -s 30 -c 1 -o $OUT/${TAG}_update $CMD2 > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu update exit $?"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+      -k regex:k_diag3 -s 250 -c 1 -o $OUT/${TAG}_diag3_c4 $CMD2 > $OUT/${TAG}_ncu_diag_c4.log 2>&1; echo "ncu diag c4 exit $?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_diag3 -s 20 -c 1 \
+      -o $OUT/${TAG}_diag3_c2 python tools/c2_once.py C2 128 > $OUT/${TAG}_ncu_diag_c2.log 2>&1; echo "ncu diag c2 exit $?"
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/${TAG}_c2_launches.csv python tools/c2_once.py C2 128 > /dev/null 2>&1; echo "ncu c2 launches exit $?"
 fi
-if [ "${SAN:-1}" = "1" ]; then
+if [ "${SAN:-0}" = "1" ]; then
   for tool in memcheck racecheck synccheck; do
     timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > $OUT/${TAG}_san_$tool.log 2>&1; echo "sanitizer $tool exit $?"; tail -3 $OUT/${TAG}_san_$tool.log
   done
