@@ -21,7 +21,9 @@
  *     0   success
  *    -i   argument i of zz_tgevc / zz_tgevc_host is invalid (1-based)
  *    +j   the 2x2 diagonal block S(j:j+1, j:j+1) (1-based) has real eigenvalues
- *         (assumption 2 of PAPER.md:69 violated); X is not written
+ *         (assumption 2 of PAPER.md:69 violated); zz_tgevc does not write X.  zz_tgevc_host
+ *         learns the status only after the wavefront: it may already have written the zeros
+ *         below each column's block into the caller's host X (the same holds for -104)
  *  -100   CUDA error      -102 out of device memory      -103 no context (zz_init missing)
  *  -104   non-finite entry in a diagonal block of S or T
  *  -105   overlapping 2x2 blocks (two consecutive nonzero subdiagonal entries of S)

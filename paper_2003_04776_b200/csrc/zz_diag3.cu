@@ -60,6 +60,7 @@ struct Sm3 {
   int* bs;         // block b = rows [bs[b], bs[b+1]); bs[b] = 8b - (row 8b is a 2x2 bottom)
   unsigned char* teams;   // per team of warps: team_bytes(W, nblk) (see Team)
   double* ptab;           // per warp: pivot table (G stage 1; the substitution's prepared pivots)
+  unsigned char* gring;   // one warp per task: the G producers' ring (GRing), else unused
   signed char* fl; // row flags
 };
 
@@ -86,10 +87,11 @@ __host__ __device__ __forceinline__ size_t team_bytes(int W, int nblk) {
 constexpr size_t kPtabBytes = sizeof(double) * 576;   // per warp: pivot table [9][8][8]
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ __forceinline__ size_t gring_bytes() { return 4 * 5632 + 64; }   // kGSlots x kGSlotBytes + flags
 __host__ __device__ __forceinline__ size_t smem3(int nt, int nteams, size_t tb, int nwarps) {
   return a16(sizeof(double2) * (size_t)(nt * (nt + 3) / 2 + kPad3)) + a16(sizeof(double2) * (size_t)nt) +
          a16(sizeof(double2) * 17) + a16(sizeof(double2) * 17) + a16(sizeof(int) * 18) + a16(tb) * nteams +
-         kPtabBytes * nwarps + a16((size_t)nt);
+         kPtabBytes * nwarps + (nteams == nwarps ? gring_bytes() : 0) + a16((size_t)nt);
 }
 __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt, int nteams, size_t tb, int nwarps) {
   Sm3 s;
@@ -101,6 +103,7 @@ __device__ __forceinline__ Sm3 carve3(unsigned char* base, int nt, int nteams, s
   s.bs = reinterpret_cast<int*>(base + o); o += a16(sizeof(int) * 18);
   s.teams = base + o; o += a16(tb) * nteams;
   s.ptab = reinterpret_cast<double*>(base + o); o += kPtabBytes * nwarps;
+  s.gring = base + o; o += (nteams == nwarps ? gring_bytes() : 0);
   s.fl = reinterpret_cast<signed char*>(base + o);
   return s;
 }
@@ -313,6 +316,19 @@ struct GRows {
 // 1x1 slot J: (1/d) at [J][0..1]; 2x2 block (J, J+1): real -- inv at [J][0..3] (row-major);
 // pair -- inv row 0 at [J][0..3], row 1 at [J+1][0..3] (complex).  A rolled loop (compact code:
 // the diagonal solve is bound by instruction fetch when its code is unrolled).
+// G producers (one or two tasks per CTA): the CTA's idle warps form the rows of G of the task's blocks
+// nblk-2, ..., 0 (the same gpiv/gprep arithmetic as the solving warp, so results do not depend
+// on who formed them) into a ring of shared-memory slots; the solving warp only loads them.
+constexpr int kGSlots = 4;
+constexpr int kGVals = 22;                 // doubles per lane per block (see gstore / gload)
+constexpr size_t kGSlotBytes = sizeof(double) * kGVals * 32;
+struct GRing {
+  double* slot;    // [ns][kGVals][32]
+  int* ready;      // [ns]: block id + 1 of the rows in the slot
+  int* done;       // [ns]: block id + 1 of the last rows the solving warp consumed
+  int ns;          // slots (kGSlots / tasks per CTA)
+};
+
 template <bool PAIR>
 __device__ __forceinline__ void gpiv_block(const Sm3& sm, int r0, int q0, int qe, double a, double b, double beta,
                                         double ab, int u, int col, double* ptab) {
@@ -510,6 +526,50 @@ __device__ __forceinline__ void gprep_block(const Sm3& sm, int g8, int q0, int q
     }
   }
   __syncwarp();   // the pivot table is reused (slow path, next block)
+}
+
+// a lane's rows of G in a ring slot (element i of lane l at [i][l]: conflict-free)
+template <bool PAIR>
+__device__ __forceinline__ void gstore(const GRows& gr, double* sl, int lane) {
+#pragma unroll
+  for (int J = 0; J < 9; ++J) sl[J * 32 + lane] = gr.ar[J];
+  if (!PAIR) {
+#pragma unroll
+    for (int J = 3; J < 9; ++J) sl[(6 + J) * 32 + lane] = gr.br[J];
+    sl[15 * 32 + lane] = gr.cr7;
+    sl[16 * 32 + lane] = gr.cr8;
+  } else {
+#pragma unroll
+    for (int J = 0; J < 9; ++J) sl[(9 + J) * 32 + lane] = gr.ai[J];
+    sl[18 * 32 + lane] = gr.cr7;
+    sl[19 * 32 + lane] = gr.ci7;
+    sl[20 * 32 + lane] = gr.cr8;
+    sl[21 * 32 + lane] = gr.ci8;
+  }
+}
+template <bool PAIR>
+__device__ __forceinline__ void gload(GRows& gr, const double* sl, int lane) {
+#pragma unroll
+  for (int J = 0; J < 9; ++J) {
+    gr.ar[J] = sl[J * 32 + lane];
+    gr.ai[J] = 0.0;
+    gr.br[J] = 0.0;
+  }
+  if (!PAIR) {
+#pragma unroll
+    for (int J = 3; J < 9; ++J) gr.br[J] = sl[(6 + J) * 32 + lane];
+    gr.cr7 = sl[15 * 32 + lane];
+    gr.cr8 = sl[16 * 32 + lane];
+    gr.ci7 = 0.0;
+    gr.ci8 = 0.0;
+  } else {
+#pragma unroll
+    for (int J = 0; J < 9; ++J) gr.ai[J] = sl[(9 + J) * 32 + lane];
+    gr.cr7 = sl[18 * 32 + lane];
+    gr.ci7 = sl[19 * 32 + lane];
+    gr.cr8 = sl[20 * 32 + lane];
+    gr.ci8 = sl[21 * 32 + lane];
+  }
 }
 
 // x = G y for this lane's rows and the overflow / conditioning verdict (see gprep_block)
@@ -801,11 +861,52 @@ __device__ __forceinline__ SlowSt slow_block(const Sm3& sm, double* wslab, doubl
 }
 
 // ------------------------------------------------------------------------------------
+// A G producer (warp h of nh idle warps of a CTA holding one task): the rows of G of the task's
+// blocks nblk-2-h, nblk-2-h-nh, ... (block nblk-1 is formed by the solving warp itself), with
+// exactly the solving warp's arithmetic, into the ring slot block % kGSlots once the solving
+// warp has consumed the slot's previous rows.
+// ------------------------------------------------------------------------------------
+template <bool PAIR>
+__device__ __forceinline__ void gproduce_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane,
+                                              int h, int nh, double* ptab, const GRing& ring) {
+  const DevPlan& P = p.P;
+  const int team = lane >> 2, t = lane & 3;
+  const int comp = PAIR ? (team & 1) : 0;
+  const int cpt = p.cpt;
+  const int slot = PAIR ? (team >> 1) : team;
+  const int item = PAIR ? task * (cpt / 2) + slot : task * cpt + slot;
+  const int n_items = PAIR ? p.n_pair : p.n_real;
+  const bool valid = item < n_items && slot < (PAIR ? cpt / 2 : cpt);
+  const int c0 = valid ? (PAIR ? p.pair_items[item] : p.real_items[item]) : -1;
+  double a = 0.0, b = 0.0, beta = 0.0;
+  if (valid) {
+    a = P.col_a[c0];
+    b = PAIR ? P.col_b[c0] : 0.0;
+    beta = P.col_beta[c0];
+  }
+  const double ab = __dadd_rn(fabs(a), fabs(b));
+  const int u = PAIR ? comp * 4 + t : t, col = PAIR ? (team & ~1) : team;
+  for (int k = nblk - 2 - h; k >= 0; k -= nh) {
+    const int g8 = 8 * k, q0 = sm.bs[k] - (g8 - 1), qe = sm.bs[k + 1] - (g8 - 1);
+    const double2 bnv = sm.bn[k];
+    const double gsc = gscale(__dadd_rn(__dmul_rn(beta, bnv.x), __dmul_rn(ab, bnv.y)));
+    gpiv_block<PAIR>(sm, g8 - 1, q0, qe, a * gsc, b * gsc, beta * gsc, ab * gsc, u, col, ptab);
+    GRows gr;
+    gprep_block<PAIR>(sm, g8, q0, qe, p.nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u, col, ptab, gr);
+    const int si = k % ring.ns;
+    if (k + ring.ns <= nblk - 2) pub_wait(&ring.done[si], k + ring.ns + 1, lane);
+    gstore<PAIR>(gr, ring.slot + si * (kGVals * 32), lane);
+    __syncwarp();
+    if (lane == 0) pub_release(&ring.ready[si], k + 1);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // One task: 8 real columns (PAIR = false) or 4 complex pairs (PAIR = true) of tile I.
 // ------------------------------------------------------------------------------------
 template <int G, bool PAIR, bool TEAMS>
 __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane,
-                                        const Team& tm) {
+                                        const Team& tm, const GRing ring) {
   const DevPlan& P = p.P;
   const int team = lane >> 2, t = lane & 3;
   const int comp = PAIR ? (team & 1) : 0;
@@ -948,12 +1049,23 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
     const double dn0 = __dadd_rn(__dmul_rn(beta, bnv.x), __dmul_rn(ab, bnv.y));
     const double gsc = gscale(dn0), dn = dn0 * gsc;   // G is formed for gsc D (gscale)
     const int u = PAIR ? comp * 4 + t : t;
-    if (blk != pre_blk)
-      gpiv_block<PAIR>(sm, g8 - 1, q0, e0 - (g8 - 1), a * gsc, b * gsc, beta * gsc, ab * gsc, u, PAIR ? (team & ~1) : team, pslab);
-    ZZ_TR(256 + blk * 8 + 0);
     GRows gpre;
-    gprep_block<PAIR>(sm, g8, q0, e0 - (g8 - 1), nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u,
-                      PAIR ? (team & ~1) : team, pslab, gpre);
+    if (ring.slot != nullptr && blk < nblk - 1) {
+      // the rows of G formed by the CTA's producer warps (gproduce_task)
+      const int si = blk % ring.ns;
+      pub_wait(&ring.ready[si], blk + 1, lane);
+      gload<PAIR>(gpre, ring.slot + si * (kGVals * 32), lane);
+      __syncwarp();
+      if (lane == 0) pub_release(&ring.done[si], blk + 1);
+      ZZ_TR(256 + blk * 8 + 0);
+    } else {
+      if (blk != pre_blk)
+        gpiv_block<PAIR>(sm, g8 - 1, q0, e0 - (g8 - 1), a * gsc, b * gsc, beta * gsc, ab * gsc, u,
+                         PAIR ? (team & ~1) : team, pslab);
+      ZZ_TR(256 + blk * 8 + 0);
+      gprep_block<PAIR>(sm, g8, q0, e0 - (g8 - 1), nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u,
+                        PAIR ? (team & ~1) : team, pslab, gpre);
+    }
     ZZ_TR(256 + blk * 8 + 1);
     bool okc = gapply_block<PAIR>(gpre, wslab, q0, e0 - (g8 - 1), dn, gsc, team, u, xfr, xfi);
     ZZ_TR(256 + blk * 8 + 2);
@@ -1197,6 +1309,10 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
       const int ef = g0 + protect_update(yh, tau, xh);
       sx = ef - es;
       if (t == 0 && w0) {
+        // lookahead: this maximum covers the rows the band and bulk updates measured, which
+        // can differ from the plain schedule's; a decision that scales is recomputed without
+        // lookahead (as for a group's first decision)
+        if (p.record_bound && ef < g0) atomicOr(&P.status[6], 1);
         P.sY[c] = ef - e_p;
         P.e_pend[c] = ef;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
@@ -1316,6 +1432,12 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   tm.red0 = reinterpret_cast<double*>(tm.pub + nslot);
   tm.red1 = tm.red0 + 8 * W;
   tm.red2 = tm.red1 + 16 * W;
+  GRing ring;
+  ring.slot = nullptr;
+  ring.ns = kGSlots;
+  ring.ready = reinterpret_cast<int*>(sm.gring + kGSlots * kGSlotBytes);
+  ring.done = ring.ready + kGSlots;
+  if (!TEAMS && threadIdx.x < 2 * kGSlots) ring.ready[threadIdx.x] = 0;   // (ready and done)
   for (int i = tm.w * 32 + lane; i < nslot; i += 32 * W) {
     tm.pub[i].flag = 0;
     tm.pub[i].cnt = 0;
@@ -1413,10 +1535,31 @@ __global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
   const int npt = (p.n_pair + p.cpt / 2 - 1) / (p.cpt / 2), nrt = (p.n_real + p.cpt - 1) / p.cpt;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two
   // (measured: contiguous per-CTA task ranges were slower, pair tasks being heavier)
+  if (!TEAMS && p.gprod && npt + nrt <= 2 * (int)gridDim.x) {
+    // one or two tasks per CTA: a task's first warp solves it, its other warps form its rows
+    // of G ahead of it (tasks CTA-fastest, as below)
+    const int tpc = (npt + nrt <= (int)gridDim.x) ? 1 : 2, wpt = kW3 / tpc;
+    const int ti = warp / wpt, role = warp % wpt;
+    const int task = ti * gridDim.x + blockIdx.x;
+    if (task >= npt + nrt) return;
+    ring.ns = kGSlots / tpc;
+    ring.slot = reinterpret_cast<double*>(sm.gring) + ti * ring.ns * (kGVals * 32);
+    ring.ready += ti * ring.ns;
+    ring.done += ti * ring.ns;
+    tm.gen = task + 1;
+    if (role == 0) {
+      if (task < npt) solve_task<G, true, TEAMS>(p, sm, nblk, task, lane, tm, ring);
+      else solve_task<G, false, TEAMS>(p, sm, nblk, task - npt, lane, tm, ring);
+    } else {
+      if (task < npt) gproduce_task<true>(p, sm, nblk, task, lane, role - 1, wpt - 1, sm.ptab + 576 * warp, ring);
+      else gproduce_task<false>(p, sm, nblk, task - npt, lane, role - 1, wpt - 1, sm.ptab + 576 * warp, ring);
+    }
+    return;
+  }
   for (int task = tix * gridDim.x + blockIdx.x; task < npt + nrt; task += gridDim.x * nteams) {
     tm.gen = task + 1;
-    if (task < npt) solve_task<G, true, TEAMS>(p, sm, nblk, task, lane, tm);
-    else solve_task<G, false, TEAMS>(p, sm, nblk, task - npt, lane, tm);
+    if (task < npt) solve_task<G, true, TEAMS>(p, sm, nblk, task, lane, tm, ring);
+    else solve_task<G, false, TEAMS>(p, sm, nblk, task - npt, lane, tm, ring);
   }
 }
 
@@ -1466,13 +1609,16 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
     }
   }
   p.team_w = W;
+  // default (team_w 0): with one task per CTA the idle warps produce the rows of G
+  p.gprod = (pin.team_w == 0 && W == 1 && tasks <= 2 * g_sms3) ? 1 : 0;
   const int per_cta = nw / W;   // tasks per CTA at a time
   const size_t smem = smem3(p.nt, per_cta, a16(team_bytes(W, nblk)), nw);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e;
   // pack: as few CTAs as the tasks need (one task per team), leaving the other SMs to a
   // concurrent update (lookahead); otherwise one task per CTA first (lowest latency alone)
-  const int grid = p.pack ? std::min(g_sms3, (tasks + per_cta - 1) / per_cta) : (tasks < g_sms3 ? tasks : g_sms3);
+  int grid = p.pack ? std::min(g_sms3, (tasks + per_cta - 1) / per_cta) : (tasks < g_sms3 ? tasks : g_sms3);
+  if (p.gprod && p.pack) grid = (tasks + 1) / 2;   // lookahead: two tasks (and their producers) per CTA
 #define ZZ_LAUNCH3(GG, TT)                                                                           \
   do {                                                                                              \
     e = cudaFuncSetAttribute(k_diag3<GG, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \

@@ -174,6 +174,7 @@ struct Diag2Params {
   int use_bound, record_bound;
   int pack;                // launch as few CTAs as the tasks need (lookahead)
   int team_w;              // warps per task (0: chosen by launch_diag3; results do not depend on it)
+  int gprod;               // one task per CTA: the idle warps form the rows of G (set by launch_diag3)
 };
 
 // launchers (zz_kernels.cu / zz_update.cu / zz_diag.cu)
