@@ -574,7 +574,7 @@ __device__ __forceinline__ void gload(GRows& gr, const double* sl, int lane) {
 
 // x = G y for this lane's rows and the overflow / conditioning verdict (see gprep_block)
 template <bool PAIR>
-__device__ __forceinline__ bool gapply_block(const GRows& gr, const double* wslab, int q0, int qe, double dn,
+__device__ __forceinline__ bool gapply_block(const GRows& gr, const double* wslab, int q0, int qe, int tq, double dn,
                                              double sc, int team, int u, double (&xr)[3], double (&xi)[3]) {
   const int qB = PAIR ? 99 : u + 4, qA = u;
   const bool hasC = (u == 0) && qe == 9;
@@ -586,7 +586,7 @@ __device__ __forceinline__ bool gapply_block(const GRows& gr, const double* wsla
   double xar = 0.0, xai = 0.0, xbr = 0.0, xcr = 0.0, xci = 0.0;
 #pragma unroll
   for (int J = 0; J < 9; ++J) {
-    if (J >= q0 && J < qe) {
+    if (J >= q0 && J < qe && J < tq) {   // (a tip block: the leading rows only)
       const double yr = wslab[J * 8 + pt], yi = PAIR ? wslab[J * 8 + pt + 1] : 0.0;
       ymax = dmaxd(ymax, PAIR ? dmaxd(fabs(yr), fabs(yi)) : fabs(yr));
       if (!PAIR) {
@@ -1067,11 +1067,48 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
                         PAIR ? (team & ~1) : team, pslab, gpre);
     }
     ZZ_TR(256 + blk * 8 + 1);
-    bool okc = gapply_block<PAIR>(gpre, wslab, q0, e0 - (g8 - 1), dn, gsc, team, u, xfr, xfi);
+    // ---- the tip's own block (Kernel 1; reading R10): the eigenvalue rows get the tip
+    // values, the rows above them in the block are x = G y with G restricted to the leading
+    // rows (its entries there do not involve the singular pivot) and y = -D(rows, tip rows) x_tip
+    // (tips start from zero; the slab takes y, and back the zeros if the substitution runs) ----
+    const bool tipblk = tip && tipr >= s0 && tipr < e0;
+    int tq = 99;
+    cpx xt0 = mkc(0.0, 0.0), xt1 = mkc(0.0, 0.0);
+    if (tipblk) {
+      const int rr = tipr, top = PAIR ? rr - 1 : rr;
+      tq = top - (g8 - 1);
+      if (!PAIR) {
+        xt0 = mkc(1.0, 0.0);
+      } else {
+        const double2 d21 = sm.ST[poff3(rr - 1) + rr], d22 = sm.ST[poff3(rr) + rr];
+        const double pp = __dmul_rn(beta, d21.x);
+        const cpx qq = mkc(__fma_rn(-a, d22.y, __dmul_rn(beta, d22.x)), __dmul_rn(-b, d22.y));
+        if (fabs(pp) >= n1(qq)) {
+          xt1 = mkc(1.0, 0.0);
+          xt0 = mkc(__ddiv_rn(-qq.re, pp), __ddiv_rn(-qq.im, pp));
+        } else {
+          xt0 = mkc(1.0, 0.0);
+          const cpx z = cdivx(mkc(pp, 0.0), qq);
+          xt1 = mkc(-z.re, -z.im);
+        }
+      }
+      for (int r = t; r < tq; r += 4) {   // slot r of the column: lane r & 3
+        if (r < q0) continue;
+        const int j = g8 - 1 + r;
+        const double2 f0 = sm.ST[poff3(top) + j];
+        cpx yv = cmulx(mkc(__fma_rn(-a, f0.y, __dmul_rn(beta, f0.x)), __dmul_rn(-b, f0.y)), xt0);
+        if (PAIR) {
+          const double2 f1 = sm.ST[poff3(rr) + j];
+          const cpx d1 = mkc(__fma_rn(-a, f1.y, __dmul_rn(beta, f1.x)), __dmul_rn(-b, f1.y));
+          const cpx p1 = cmulx(d1, xt1);
+          yv = mkc(__dadd_rn(yv.re, p1.re), __dadd_rn(yv.im, p1.im));
+        }
+        wslab[r * 8 + team] = PAIR ? (comp ? -yv.im : -yv.re) : -yv.re;
+      }
+    }
+    __syncwarp();
+    bool okc = gapply_block<PAIR>(gpre, wslab, q0, e0 - (g8 - 1), tq, dn, gsc, team, u, xfr, xfi);
     ZZ_TR(256 + blk * 8 + 2);
-#ifndef ZZ_VARIANT_NOTIP
-    okc = okc && !(tip && tipr >= s0 && tipr < e0);
-#endif
 #ifdef ZZ_VARIANT_NOFAST
     okc = false;
 #endif
@@ -1084,6 +1121,8 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
     }
     int kseg = 0;
     ZZ_TR(blk * 8 + 1);
+    if (tipblk && !okc)   // the substitution starts the tip from zero itself
+      for (int r = t; r < tq; r += 4) wslab[r * 8 + team] = 0.0;
     if (__any_sync(0xffffffffu, !okc)) {
     const double bound0 = bound;
     const int ex0 = ex;
@@ -1103,6 +1142,17 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
     if (okc) {
       const int qe = e0 - (g8 - 1);
       const int pt = PAIR ? (team & ~1) : team;
+      if (tipblk) {   // the tip rows and the zeros below them
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = (i == 0) ? u : (i == 1 ? u + 4 : 8);
+          const cpx v = (q == tq) ? xt0 : ((PAIR && q == tq + 1) ? xt1 : mkc(0.0, 0.0));
+          if (q >= tq) {
+            xfr[i] = v.re;
+            xfi[i] = v.im;
+          }
+        }
+      }
       double xm = 0.0;
       if (u >= q0 && u < qe) {
         wslab[u * 8 + pt] = xfr[0];
