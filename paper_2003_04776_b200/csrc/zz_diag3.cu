@@ -1460,9 +1460,11 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
   ZZ_TR(160 + w);
 }
 
-template <int G, bool TEAMS>
-__global__ void __launch_bounds__(W3<G>::n * 32, 1) k_diag3(Diag2Params p) {
-  constexpr int kW3 = W3<G>::n;
+// NW warps per CTA: W3<G>::n (12 or 16) in general; 8 with G producers (one or two tasks per
+// CTA, up to 255 registers per thread: no spills in the solving warp)
+template <int G, bool TEAMS, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_diag3(Diag2Params p) {
+  constexpr int kW3 = NW;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int nt = p.nt;
   ZZ_TR0();
@@ -1661,26 +1663,33 @@ cudaError_t launch_diag3(const Diag2Params& pin, cudaStream_t st) {
   p.team_w = W;
   // default (team_w 0): with one task per CTA the idle warps produce the rows of G
   p.gprod = (pin.team_w == 0 && W == 1 && tasks <= 2 * g_sms3) ? 1 : 0;
-  const int per_cta = nw / W;   // tasks per CTA at a time
-  const size_t smem = smem3(p.nt, per_cta, a16(team_bytes(W, nblk)), nw);
+#ifdef ZZ_VARIANT_NW8
+  const int nwl = 8;
+#else
+  const int nwl = p.gprod ? 8 : nw;   // warps per CTA of this launch
+#endif
+  const int per_cta = nwl / W;        // tasks per CTA at a time
+  const size_t smem = smem3(p.nt, per_cta, a16(team_bytes(W, nblk)), nwl);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e;
   // pack: as few CTAs as the tasks need (one task per team), leaving the other SMs to a
   // concurrent update (lookahead); otherwise one task per CTA first (lowest latency alone)
   int grid = p.pack ? std::min(g_sms3, (tasks + per_cta - 1) / per_cta) : (tasks < g_sms3 ? tasks : g_sms3);
   if (p.gprod && p.pack) grid = (tasks + 1) / 2;   // lookahead: two tasks (and their producers) per CTA
-#define ZZ_LAUNCH3(GG, TT)                                                                           \
-  do {                                                                                              \
-    e = cudaFuncSetAttribute(k_diag3<GG, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
-    if (e != cudaSuccess) return e;                                                                 \
-    k_diag3<GG, TT><<<grid, nw * 32, smem, st>>>(p);                                                \
+#define ZZ_LAUNCH3(GG, TT, NN)                                                                           \
+  do {                                                                                                  \
+    e = cudaFuncSetAttribute(k_diag3<GG, TT, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
+    if (e != cudaSuccess) return e;                                                                     \
+    k_diag3<GG, TT, NN><<<grid, NN * 32, smem, st>>>(p);                                                \
   } while (0)
   if (small) {
-    if (W > 1) ZZ_LAUNCH3(8, true);
-    else ZZ_LAUNCH3(8, false);
+    if (W > 1) ZZ_LAUNCH3(8, true, W3<8>::n);
+    else if (p.gprod || nwl == 8) ZZ_LAUNCH3(8, false, 8);
+    else ZZ_LAUNCH3(8, false, W3<8>::n);
   } else {
-    if (W > 1) ZZ_LAUNCH3(16, true);
-    else ZZ_LAUNCH3(16, false);
+    if (W > 1) ZZ_LAUNCH3(16, true, W3<16>::n);
+    else if (p.gprod || nwl == 8) ZZ_LAUNCH3(16, false, 8);
+    else ZZ_LAUNCH3(16, false, W3<16>::n);
   }
 #undef ZZ_LAUNCH3
   return cudaGetLastError();
