@@ -316,9 +316,9 @@ struct GRows {
 // 1x1 slot J: (1/d) at [J][0..1]; 2x2 block (J, J+1): real -- inv at [J][0..3] (row-major);
 // pair -- inv row 0 at [J][0..3], row 1 at [J+1][0..3] (complex).  A rolled loop (compact code:
 // the diagonal solve is bound by instruction fetch when its code is unrolled).
-// G producers (one or two tasks per CTA): the CTA's idle warps form the rows of G of the task's blocks
-// nblk-2, ..., 0 (the same gpiv/gprep arithmetic as the solving warp, so results do not depend
-// on who formed them) into a ring of shared-memory slots; the solving warp only loads them.
+// G producers (one or two tasks per CTA): the CTA's idle warps form the rows of G of the task's
+// blocks (the same gpiv/gprep arithmetic as the solving warp, so results do not depend on who
+// formed them) into a ring of shared-memory slots; the solving warp only loads them.
 constexpr int kGSlots = 4;
 constexpr int kGVals = 22;                 // doubles per lane per block (see gstore / gload)
 constexpr size_t kGSlotBytes = sizeof(double) * kGVals * 32;
@@ -861,10 +861,10 @@ __device__ __forceinline__ SlowSt slow_block(const Sm3& sm, double* wslab, doubl
 }
 
 // ------------------------------------------------------------------------------------
-// A G producer (warp h of nh idle warps of a CTA holding one task): the rows of G of the task's
-// blocks nblk-2-h, nblk-2-h-nh, ... (block nblk-1 is formed by the solving warp itself), with
-// exactly the solving warp's arithmetic, into the ring slot block % kGSlots once the solving
-// warp has consumed the slot's previous rows.
+// A G producer (warp h of nh idle warps of a CTA holding one or two tasks): the rows of G of the
+// task's blocks nblk-1-h, nblk-1-h-nh, ... (the first while the solving warp loads its
+// right-hand side), with exactly the solving warp's arithmetic, into the ring slot block % ns
+// once the solving warp has consumed the slot's previous rows.
 // ------------------------------------------------------------------------------------
 template <bool PAIR>
 __device__ __forceinline__ void gproduce_task(const Diag2Params& p, const Sm3& sm, int nblk, int task, int lane,
@@ -886,7 +886,7 @@ __device__ __forceinline__ void gproduce_task(const Diag2Params& p, const Sm3& s
   }
   const double ab = __dadd_rn(fabs(a), fabs(b));
   const int u = PAIR ? comp * 4 + t : t, col = PAIR ? (team & ~1) : team;
-  for (int k = nblk - 2 - h; k >= 0; k -= nh) {
+  for (int k = nblk - 1 - h; k >= 0; k -= nh) {
     const int g8 = 8 * k, q0 = sm.bs[k] - (g8 - 1), qe = sm.bs[k + 1] - (g8 - 1);
     const double2 bnv = sm.bn[k];
     const double gsc = gscale(__dadd_rn(__dmul_rn(beta, bnv.x), __dmul_rn(ab, bnv.y)));
@@ -894,7 +894,7 @@ __device__ __forceinline__ void gproduce_task(const Diag2Params& p, const Sm3& s
     GRows gr;
     gprep_block<PAIR>(sm, g8, q0, qe, p.nt, a * gsc, b * gsc, beta * gsc, ab * gsc, u, col, ptab, gr);
     const int si = k % ring.ns;
-    if (k + ring.ns <= nblk - 2) pub_wait(&ring.done[si], k + ring.ns + 1, lane);
+    if (k + ring.ns <= nblk - 1) pub_wait(&ring.done[si], k + ring.ns + 1, lane);
     gstore<PAIR>(gr, ring.slot + si * (kGVals * 32), lane);
     __syncwarp();
     if (lane == 0) pub_release(&ring.ready[si], k + 1);
@@ -1050,7 +1050,7 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
     const double gsc = gscale(dn0), dn = dn0 * gsc;   // G is formed for gsc D (gscale)
     const int u = PAIR ? comp * 4 + t : t;
     GRows gpre;
-    if (ring.slot != nullptr && blk < nblk - 1) {
+    if (ring.slot != nullptr) {
       // the rows of G formed by the CTA's producer warps (gproduce_task)
       const int si = blk % ring.ns;
       pub_wait(&ring.ready[si], blk + 1, lane);
@@ -1524,6 +1524,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_diag3(Diag2Params p) {
     else if (b > 0 && sm.fl[v] == kRowBot2) v -= 1;
     sm.bs[b] = v;
   }
+#ifdef ZZ_VARIANT_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[181] = clock64();
+#endif
   // in-tile column bounds above each block (reading R6)
   for (int j = threadIdx.x; j < nt; j += blockDim.x) {
     const int top = (sm.fl[j] == kRowBot2) ? j - 1 : j;
@@ -1583,6 +1586,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_diag3(Diag2Params p) {
     if (lane == 0) sm.bn[b] = make_double2(bs_, bt_);
   }
   __syncthreads();
+#ifdef ZZ_VARIANT_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[182] = clock64();
+#endif
   // ---- tasks (4 complex pairs or 8 real columns), one per team of W warps ----
   const int npt = (p.n_pair + p.cpt / 2 - 1) / (p.cpt / 2), nrt = (p.n_real + p.cpt - 1) / p.cpt;
   // CTA-fastest assignment: with few tasks every SM gets one before any SM gets two

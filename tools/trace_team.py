@@ -22,6 +22,7 @@ for W in [int(w) for w in os.environ.get("TEAMS", "1,12").split(",")]:
     t0 = tr[180]
     rel = lambda v: (v - t0) if v else -1
     print("W=%d  (cycles from kernel start)" % W)
+    print("  staged", rel(tr[181]), "bounds", rel(tr[182]))
     print("  init  ", [rel(tr[200 + w]) for w in range(12)])
     print("  chain0", [rel(tr[220 + w]) for w in range(12)])
     for k in range(15, -1, -1):
