@@ -28,13 +28,19 @@ constexpr int kABytes = kBM * kBK * 8;     // S or T chunk: [BM/8][BK][8] double
 constexpr int kBBytes = kBN * kBK * 8;     // W chunk:      [BK/4][BN][4] doubles
 constexpr int kNGroup = 64;                // N tiles per group of the CTA order (tile_coords)
 
-// 2 (rows) x 2 (columns) consumer warps of 64 x 32 consume a 128 x 64 tile; one producer warp
+// 2 (rows) x 2 (columns) consumer warps of 64 x 32 consume a 128 x 64 tile; one producer warp.
+// BMC = 64 / 32: half / quarter tiles (warps of 32 / 16 rows x 32) for launches with fewer
+// CTAs than SMs (thin band updates, small steps): more CTAs, each at the full DMMA rate of its
+// SM, and the same DMMA sequence per accumulator, so bitwise the same result.
+template <int BMC = kBM>
 struct UT {
   static constexpr int BN = 64;
   static constexpr int CW = 4;                              // consumer warps
+  static constexpr int MI = BMC / 16;                       // 8-row blocks per consumer warp
   static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int ABYTES = BMC * kBK * 8;
   static constexpr int BBYTES = BN * kBK * 8;
-  static constexpr int STAGE = kABytes + BBYTES;
+  static constexpr int STAGE = ABYTES + BBYTES;
   static constexpr int SMEM = kStages * STAGE + 2 * kStages * 8 + BN * 8;
 };
 
@@ -56,15 +62,15 @@ __device__ __forceinline__ void tile_coords(int tile, int n_mtiles, int n_ntl, i
   ntl = g * ng + loc % gs;
 }
 
-template <int MODE = 0>
-__global__ void __launch_bounds__(UT::THREADS, 2)
+template <int MODE = 0, int BMC = kBM>
+__global__ void __launch_bounds__(UT<BMC>::THREADS, 2)
     k_update_t(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmT, UpdParams p,
                int n_mtiles, int n_tiles) {
-  using C = UT;
+  using C = UT<BMC>;
   constexpr int WN = 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
-  double* sB = reinterpret_cast<double*>(smem + kStages * kABytes);
+  double* sB = reinterpret_cast<double*>(smem + kStages * C::ABYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::STAGE);
   uint64_t* empty = full + kStages;
   unsigned long long* colmax = reinterpret_cast<unsigned long long*>(empty + kStages);
@@ -104,13 +110,13 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
         const int tile = blockIdx.x;
         int mt, ntl;
         tile_coords(tile, n_mtiles, n_ntl, kNGroup, mt, ntl);
-        const int m0 = mbase + mt * kBM;
+        const int m0 = mbase + mt * BMC;
         const int nb64 = p.ntile0 + ntl * (C::BN / kBN);   // first 64-column block
         const int nblk = min(C::BN / kBN, p.ntile_end - nb64);         // 64-column blocks present
         for (int kc = 0; kc < nkc; ++kc, ++g) {
           const int s = g % kStages;
           if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
-          mbar_expect_tx(&full[s], kABytes + nblk * kBBytes);
+          mbar_expect_tx(&full[s], C::ABYTES + nblk * kBBytes);
           // segment of chunk kc (static indices: the parameter arrays stay in constant space)
           int kl = kc, nks_s = p.nks, t0_s = p.t0;
           const double* w_s = p.W;
@@ -132,10 +138,10 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
           }
           const CUtensorMap* tm = (kl < nks_s) ? &tmS : &tmT;
           const int kcol = t0_s + (kl % nks_s) * kBK;
-          double* a = sA + s * (kBM * kBK);
-          // S/T chunk as [BM/8][BK][8]: 16 TMA boxes of 8 rows x 16 columns
+          double* a = sA + s * (BMC * kBK);
+          // S/T chunk as [BM/8][BK][8]: 16 (8) TMA boxes of 8 rows x 16 columns
 #pragma unroll 4
-          for (int mo = 0; mo < kBM / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
+          for (int mo = 0; mo < BMC / 8; ++mo) tma_load_2d(a + mo * (kBK * 8), tm, m0 + mo * 8, kcol, &full[s]);
           for (int q = 0; q < nblk; ++q)
             bulk_load_h(sB + s * (C::BN * kBK) + q * (kBN * kBK),
                         w_s + (long long)(nb64 + q) * ((long long)(2 * nks_s) * (kBN * kBK)) +
@@ -157,9 +163,10 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
     const int tile = blockIdx.x;
     int mt, ntl;
     tile_coords(tile, n_mtiles, n_ntl, kNGroup, mt, ntl);
-    const int m0 = mbase + mt * kBM;
+    const int m0 = mbase + mt * BMC;
     const int n0 = (p.ntile0 + ntl * (C::BN / kBN)) * kBN;
-    double acc[4][8][2];
+    constexpr int MI = C::MI;
+    double acc[4][MI][2];
     // accumulators start from the scaled pending values 2^sY[c] Y (exact): all loads first
     int sy[4];
 #pragma unroll
@@ -172,8 +179,8 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
       // one 16-byte load per row pair (X is 16-byte aligned with an even ldx on this path),
       // all issued before any is consumed
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      for (int mi = 0; mi < MI; ++mi) {
+        const int i0 = m0 + wm * (BMC / 2) + mi * 8 + 2 * rq;
         acc[ni][mi][0] = 0.0;
         acc[ni][mi][1] = 0.0;
         // a pair straddling the last row is loaded whole (row p.rows exists: p.rows < m <=
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
     for (int ni = 0; ni < 4; ++ni) {
       if (sy[ni] != 0) {
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
+        for (int mi = 0; mi < MI; ++mi) {
           acc[ni][mi][0] = ldexp(acc[ni][mi][0], sy[ni]);
           acc[ni][mi][1] = ldexp(acc[ni][mi][1], sy[ni]);
         }
@@ -203,19 +210,19 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
       // chunks).  Every DMMA of chunk kc-1 has issued -- its fragments have landed -- before
       // this point.  (The last kStages chunks have no refill to release.)
       if (lane == 0 && kc >= 1 && kc - 1 + kStages < nkc) mbar_arrive(&empty[(g - 1) % kStages]);
-      const double* a = sA + s * (kBM * kBK);
+      const double* a = sA + s * (BMC * kBK);
       const double* b = bw + s * (C::BN * kBK);
 #pragma unroll
       for (int ks = 0; ks < kBK / 4; ++ks) {
-        double fw[4], fs[8];
+        double fw[4], fs[MI];
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) fw[ni] = b[(ks * kBN + wc + ni * 8 + cq) * 4 + rq];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) fs[mi] = a[((wm * 8 + mi) * kBK + ks * 4 + rq) * 8 + cq];
+        for (int mi = 0; mi < MI; ++mi) fs[mi] = a[((wm * MI + mi) * kBK + ks * 4 + rq) * 8 + cq];
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-          for (int mi = 0; mi < 8; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
+          for (int mi = 0; mi < MI; ++mi) dmma(acc[ni][mi][0], acc[ni][mi][1], fw[ni], fs[mi]);
       }
       __syncwarp();
     }
@@ -228,8 +235,8 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
       double* xc = p.X + (long long)(cvalid ? c : 0) * p.ldx;
       double cm = 0.0;
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const int i0 = m0 + wm * 64 + mi * 8 + 2 * rq;
+      for (int mi = 0; mi < MI; ++mi) {
+        const int i0 = m0 + wm * (BMC / 2) + mi * 8 + 2 * rq;
         const double v0 = acc[ni][mi][0], v1 = acc[ni][mi][1];
         // rows [row_lo, rows) only: a pair may straddle either end
         const bool both = cvalid && (i0 + 1 < p.rows) && (i0 >= row_lo);
@@ -256,21 +263,41 @@ __global__ void __launch_bounds__(UT::THREADS, 2)
 }
 
 
-template <int MODE>
-static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
-                            cudaStream_t st) {
+static int g_sms_u = 0;
+
+template <int MODE, int BMC>
+static cudaError_t launch_tt(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
+                             cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_update_t<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, UT::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_update_t<MODE, BMC>, cudaFuncAttributeMaxDynamicSharedMemorySize, UT<BMC>::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_update_t<MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(k_update_t<MODE, BMC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   p.ntile_end = p.ntile0 + n_ntiles64;
   const int n_tiles = n_mtiles * n_ntiles64;   // one (m-tile, n-tile) per CTA
-  k_update_t<MODE><<<n_tiles, UT::THREADS, UT::SMEM, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
+  k_update_t<MODE, BMC><<<n_tiles, UT<BMC>::THREADS, UT<BMC>::SMEM, st>>>(*tmS, *tmT, p, n_mtiles, n_tiles);
   return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_t(const CUtensorMap* tmS, const CUtensorMap* tmT, UpdParams p, int n_mtiles, int n_ntiles64,
+                            cudaStream_t st) {
+  if (!g_sms_u) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms_u, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (n_mtiles * n_ntiles64 < g_sms_u) {
+    // fewer CTAs than SMs: half (quarter) tiles, twice (four times) the CTAs
+    const int mbase = ((MODE >= 2) ? p.row_lo : 0) & ~1;
+    const int n_m64 = (p.rows - mbase + 63) / 64;
+    if (n_m64 * n_ntiles64 < g_sms_u) return launch_tt<MODE, 32>(tmS, tmT, p, (p.rows - mbase + 31) / 32, n_ntiles64, st);
+    return launch_tt<MODE, 64>(tmS, tmT, p, n_m64, n_ntiles64, st);
+  }
+  return launch_tt<MODE, kBM>(tmS, tmT, p, n_mtiles, n_ntiles64, st);
 }
 
 // MODE 0: one step; 1: a step group's update (further K segments); 2: thin update of a band
