@@ -153,7 +153,9 @@ int zz_set_timing(int on);
  * pairs; 3 = triples; 4 = the default; up to 6).  Results differ only by summation order and by
  * how conservative the scaling bounds are (DESIGN.md s.6); groups are fixed by the tile
  * index, so results never depend on `select`.  Tiles of more than 128 rows always run
- * ungrouped.  Returns 0, -1 (k not in 1..6) or -103. */
+ * ungrouped.  zz_ztgevc groups min(k, 4) steps (its decisions use the pending bound, so
+ * they are those of the ungrouped schedule; results differ by summation order only).
+ * Returns 0, -1 (k not in 1..6) or -103. */
 int zz_set_fusion(int k);
 
 /* Lookahead schedule: the chain of diagonal solves of a step group runs on a high-priority
@@ -161,7 +163,7 @@ int zz_set_fusion(int k);
  * first decision of a group then uses a recorded upper bound of the pending rows instead of
  * their measured maximum; where that bound would make it scale, the call is recomputed
  * without lookahead (zz_info_t.lookahead_redo), so results are always those of the plain
- * schedule, bit for bit.  mode 0 = off, 1 = automatic (default: on for m >= 4096 unless a
+ * schedule, bit for bit.  mode 0 = off, 1 = automatic (default: on for m >= 1024 unless a
  * panel norm exceeds 2^64), 2 = on whenever step groups are used.  Returns 0, -1 or -103. */
 int zz_set_lookahead(int mode);
 
@@ -266,10 +268,11 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
  *                  normalisation; alpha = beta = 0 gives e_j.                  [args 7,8]
  *   col_scale_exp  DEVICE int32[n_sel] or NULL: exponents as zz_tgevc.            [arg 9]
  * Tiles of zz_set_tile() rows when it is 32, 48 or 64, else 64 (fastest,
- * profiles/r01o_complex_tile_sweep.txt).  The update of each step is one complex contraction
- * of K = 2 x tile (this library's DMMA kernel, Gauss's three-multiplication form, DESIGN.md
- * R23) over a fragment-ordered copy of the S and T panels; zz_set_lookahead(0) runs the
- * diagonal solves in line instead of on a high-priority stream.  The call
+ * profiles/r01o_complex_tile_sweep.txt).  The update of a step group (zz_set_fusion, at
+ * most 4 steps) is one complex contraction of K = 2 x tile per step (this library's DMMA
+ * kernel, Gauss's three-multiplication form, R23) over fragment-ordered copies of
+ * the S and T panels; zz_set_lookahead(0) runs the chain of diagonal solves in line instead
+ * of on a high-priority stream (bitwise the same result).  The call
  * allocates its workspace stream-ordered (cudaMallocAsync) and returns after the stream has
  * completed.  Status codes as zz_tgevc (-104 non-finite diagonal entry, -107). */
 int zz_ztgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,

@@ -576,10 +576,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   // stream `st` beside the next group's solves.  W and sY alternate between two sets by
   // group; the next group's first decision uses the recorded bound nYb instead of the
   // maximum the bulk update is still computing.
-  // (lookahead = 1, the default, is automatic: on for m >= 4096 unless a panel norm exceeds
+  // (lookahead = 1, the default, is automatic: on for m >= 1024 unless a panel norm exceeds
   // 2^64 -- then the first decisions of the groups would likely have to scale on the bound
   // and the call would be recomputed; 2 forces it, 0 disables it)
-  const bool la = can_fuse && (c->lookahead == 2 || (c->lookahead == 1 && m >= 4096 && panel_max <= 0x1p64));
+  const bool la = can_fuse && (c->lookahead == 2 || (c->lookahead == 1 && m >= 1024 && panel_max <= 0x1p64));
   cudaStream_t ms = st;
   int* sY_set[2] = {P.sY, P.sY};
   if (la) {
@@ -1307,6 +1307,8 @@ int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info) {
   *info = &c->info;
   return 0;
 }
+
+int ctx_fusion() { return g_ctx ? g_ctx->fusion : 1; }
 
 extern "C" {
 

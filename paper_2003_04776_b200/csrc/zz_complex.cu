@@ -26,6 +26,7 @@
 #include "zz_pipe.cuh"
 
 int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info);
+int ctx_fusion();
 
 namespace zz {
 namespace {
@@ -41,6 +42,7 @@ constexpr int kZBBytes = 3 * kZBK * kZBN * 8;      // 6 KB: [3][kZBK/4][32][4]
 constexpr int kZUThreads = 5 * 32;
 constexpr int kZUSmem = kZStages * (kZABytes + kZBBytes) + 2 * kZStages * 8;
 constexpr int kZNGroup = 64;    // N tiles per group of the CTA order
+constexpr int kZMaxG = 4;       // steps per step group (K segments of one update)
 
 constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag
 constexpr int kZErrNonfinite = 0;  // status key = 2*row + kind
@@ -63,6 +65,8 @@ struct ZDiagParams {
   double* W;         // update operand, k_zupdate's layout [n-tile][chunk][3 planes][2][32][4]
   int nkS;           // chunks of 8 panel columns per part (S, then T)
   int* sy;           // per column: exponent shift of the pending rows (<= 0), this step's set
+  int zero_begin;    // step groups: columns [zero_begin, cs) are not active at this step but
+                     // are in the group's fused update -- their W and sy are written as zero
 };
 
 __device__ __forceinline__ double zabsm(double2 z) { return fmax(fabs(z.x), fabs(z.y)); }
@@ -169,6 +173,19 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     Ts[idx] = r <= c ? p.T[(long long)(r0 + c) * p.ldt + r0 + r] : make_double2(0.0, 0.0);
   }
   for (int r = threadIdx.x; r < nt; r += blockDim.x) { cS[r] = p.cmS[r0 + r]; cT[r] = p.cmT[r0 + r]; }
+  if (p.zero_begin < p.cs) {
+    const int per = 16 * p.nkS;   // W rows (S part, then T part) of a column
+    const long long nz = (long long)(p.cs - p.zero_begin) * per;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nz; q += (long long)gridDim.x * blockDim.x) {
+      const int c = p.zero_begin + (int)(q / per), kk = (int)(q % per);
+      double* o = p.W + (long long)(c / kZBN) * (2 * p.nkS) * (kZBBytes / 8) + (c % kZBN) * 4 +
+                  (long long)(kk / kZBK) * (kZBBytes / 8) + ((kk % kZBK) >> 2) * (kZBN * 4) + (kk & 3);
+      o[0] = 0.0;
+      o[256] = 0.0;
+      o[512] = 0.0;
+      if (kk == 0) p.sy[c] = 0;
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * kZWarps;
@@ -360,9 +377,16 @@ struct ZUpdParams {
   int ntile0;         // first 32-column tile (c_begin / 32)
   int mtile0;         // first 64-row tile (row_lo / 64)
   double2* X; long long ldx;
-  const double* A;    // packed panel (k_zpack)
-  const double* W;    // [n-tile][nkc][3][kZBK/4][32][4]
+  // K segments (a step group, PAPER.md:235's composition over several tiles): segment e has
+  // its packed panel at A + e a_stride, its W at W + e w_stride and its sy at sy + e sy_stride,
+  // each nkc chunks.  Y <- 2^(sum_e sy_e) Y + sum_e 2^(sum_{e' < e} sy_e') A_e W_e: the
+  // contribution of tile L + e is scaled by the decisions of the later steps L + e - 1 .. L.
+  const double* A;    // packed panel (k_zpack), segment 0
+  const double* W;    // [n-tile][nkc][3][kZBK/4][32][4], segment 0
   const int* sy;
+  int nseg;
+  long long a_stride, w_stride;
+  int sy_stride;
 };
 
 // panel of step I in fragment order: block (mt, kc) = 64 rows x 8 columns x 3 planes, element
@@ -400,7 +424,8 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kZStages * (kZABytes + kZBBytes));
   uint64_t* empty = full + kZStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkc = p.nkc;
+  const int nkc = p.nkc;              // chunks per segment
+  const int nkt = p.nseg * nkc;       // chunks in all
   int mt, nt;
   {
     const int tile = blockIdx.x, per = n_mtiles * kZNGroup;
@@ -424,12 +449,16 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
       const uint64_t pol_w = l2_policy(true);
       const double* wt = p.W + (long long)ntile * nkc * (kZBBytes / 8);
       const double* at = p.A + (long long)mt * nkc * (kZABytes / 8);
-      for (int kc = 0; kc < nkc; ++kc) {
+      int e = 0, lc = 0;
+      for (int kc = 0; kc < nkt; ++kc) {
         const int s = kc % kZStages;
         if (kc >= kZStages) mbar_wait(&empty[s], ((kc / kZStages) - 1) & 1);
         mbar_expect_tx(&full[s], kZABytes + kZBBytes);
-        bulk_load_h(sA + s * (kZABytes / 8), at + (long long)kc * (kZABytes / 8), kZABytes, &full[s], pol_w);
-        bulk_load_h(sB + s * (kZBBytes / 8), wt + (long long)kc * (kZBBytes / 8), kZBBytes, &full[s], pol_w);
+        bulk_load_h(sA + s * (kZABytes / 8), at + e * p.a_stride + (long long)lc * (kZABytes / 8), kZABytes, &full[s],
+                    pol_w);
+        bulk_load_h(sB + s * (kZBBytes / 8), wt + e * p.w_stride + (long long)lc * (kZBBytes / 8), kZBBytes, &full[s],
+                    pol_w);
+        if (++lc == nkc) { lc = 0; ++e; }
       }
     }
     return;
@@ -437,13 +466,26 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
   const int wm = warp >> 1, wn = warp & 1;
   const int rq = lane & 3, cq = lane >> 2;
   const uint64_t pol_c = l2_policy(false);
+  // Per column: the exponent shift of the old Y (the sum of the group's decisions, applied in
+  // the prologue) and of each segment's W (the later steps' decisions: exact powers of two,
+  // applied to the staged fragments only in the rare case that a decision scaled).  (Holding
+  // the old Y in registers for an epilogue add needs 200 registers: 1 CTA per SM, 1.6x slower.)
   double acc1[2][4][2], acc2[2][4][2], acc3[2][4][2];
+  unsigned segscale = 0;   // warp-uniform: segments whose W some column of the warp rescales
 #pragma unroll
   for (int ni = 0; ni < 2; ++ni) {
     const int c = ntile * kZBN + wn * 16 + ni * 8 + cq;
     const bool cv = c >= p.c_begin && c < p.n_sel;
     int sy = 0;
-    ld1p_i(sy, p.sy + (cv ? c : 0), cv);
+#pragma unroll
+    for (int e = 0; e < kZMaxG; ++e) {
+      if (e < p.nseg) {
+        if (e > 0 && sy != 0) segscale |= 1u << e;
+        int v = 0;
+        ld1p_i(v, p.sy + (long long)e * p.sy_stride + (cv ? c : 0), cv);
+        sy += v;
+      }
+    }
     const double* xc = reinterpret_cast<const double*>(p.X + (long long)(cv ? c : 0) * p.ldx);
     double v[4][4];
 #pragma unroll
@@ -470,40 +512,60 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
       }
     }
   }
-  for (int kc = 0; kc < nkc; ++kc) {
+  segscale = __reduce_or_sync(0xffffffffu, segscale);
+  int e = 0, lc = 0;
+  for (int kc = 0; kc < nkt; ++kc) {
     const int s = kc % kZStages;
     mbar_wait(&full[s], (kc / kZStages) & 1);
     // release the previous stage only now (see k_update_t)
-    if (lane == 0 && kc >= 1 && kc - 1 + kZStages < nkc) mbar_arrive(&empty[(kc - 1) % kZStages]);
+    if (lane == 0 && kc >= 1 && kc - 1 + kZStages < nkt) mbar_arrive(&empty[(kc - 1) % kZStages]);
     const double* a = sA + s * (kZABytes / 8);
     const double* b = sB + s * (kZBBytes / 8);
-#pragma unroll
-    for (int ks = 0; ks < kZBK / 4; ++ks) {
-      double wr[2], wi[2], ws[2], fr[4], fi[4], fs[4];
+    // one k-step of 4 panel columns: W and panel fragments, 24 DMMAs (SCALE: the rare case of
+    // a later step in the group having scaled a column, its W fragments rescaled by 2^sc)
+#define ZZ_ZCHUNK_KS(SCALE)                                                          \
+  _Pragma("unroll") for (int ks = 0; ks < kZBK / 4; ++ks) {                          \
+    double wr[2], wi[2], ws[2], fr[4], fi[4], fs[4];                                 \
+    _Pragma("unroll") for (int ni = 0; ni < 2; ++ni) {                               \
+      const int o = (ks * kZBN + wn * 16 + ni * 8 + cq) * 4 + rq;                    \
+      wr[ni] = b[o];                                                                 \
+      wi[ni] = b[256 + o];                                                           \
+      ws[ni] = b[512 + o];                                                           \
+      if (SCALE) {                                                                   \
+        wr[ni] = ldexp(wr[ni], sc[ni]);                                              \
+        wi[ni] = ldexp(wi[ni], sc[ni]);                                              \
+        ws[ni] = ldexp(ws[ni], sc[ni]);                                              \
+      }                                                                              \
+    }                                                                                \
+    _Pragma("unroll") for (int mi = 0; mi < 4; ++mi) {                               \
+      const int g = wm * 4 + mi;                                                     \
+      fr[mi] = a[((g * 3 + 0) * 2 + ks) * 32 + lane];                                \
+      fi[mi] = a[((g * 3 + 1) * 2 + ks) * 32 + lane];                                \
+      fs[mi] = a[((g * 3 + 2) * 2 + ks) * 32 + lane];                                \
+    }                                                                                \
+    _Pragma("unroll") for (int ni = 0; ni < 2; ++ni)                                 \
+      _Pragma("unroll") for (int mi = 0; mi < 4; ++mi) {                             \
+        dmma(acc1[ni][mi][0], acc1[ni][mi][1], wr[ni], fr[mi]);                      \
+        dmma(acc2[ni][mi][0], acc2[ni][mi][1], wi[ni], fi[mi]);                      \
+        dmma(acc3[ni][mi][0], acc3[ni][mi][1], ws[ni], fs[mi]);                      \
+      }                                                                              \
+  }
+    if (!((segscale >> e) & 1)) {
+      const int sc[2] = {0, 0};
+      ZZ_ZCHUNK_KS(false)
+    } else {   // rare: the prefix sum of the earlier segments' sy, reloaded
+      int sc[2] = {0, 0};
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) {
-        const int o = (ks * kZBN + wn * 16 + ni * 8 + cq) * 4 + rq;
-        wr[ni] = b[o];
-        wi[ni] = b[256 + o];
-        ws[ni] = b[512 + o];
+        const int c = ntile * kZBN + wn * 16 + ni * 8 + cq;
+        if (c >= p.c_begin && c < p.n_sel)
+          for (int q = 0; q < e; ++q) sc[ni] += p.sy[(long long)q * p.sy_stride + c];
       }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int g = wm * 4 + mi;
-        fr[mi] = a[((g * 3 + 0) * 2 + ks) * 32 + lane];
-        fi[mi] = a[((g * 3 + 1) * 2 + ks) * 32 + lane];
-        fs[mi] = a[((g * 3 + 2) * 2 + ks) * 32 + lane];
-      }
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
-          dmma(acc1[ni][mi][0], acc1[ni][mi][1], wr[ni], fr[mi]);
-          dmma(acc2[ni][mi][0], acc2[ni][mi][1], wi[ni], fi[mi]);
-          dmma(acc3[ni][mi][0], acc3[ni][mi][1], ws[ni], fs[mi]);
-        }
+      ZZ_ZCHUNK_KS(true)
     }
+#undef ZZ_ZCHUNK_KS
     __syncwarp();
+    if (++lc == nkc) { lc = 0; ++e; }
   }
 #pragma unroll
   for (int ni = 0; ni < 2; ++ni) {
@@ -622,16 +684,25 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   const double2* T = reinterpret_cast<const double2*>(T_);
   double2* X = reinterpret_cast<double2*>(X_);
   if (n == 0) return 0;
+  // Step groups (zz_set_fusion, at most kZMaxG steps): the steps of a group I, I-1, ..., L run
+  // their diagonal solves, each followed by a thin update of the group's remaining band (the
+  // rows of tiles L .. X-1) with W_X, and then ONE update of all rows above tile L with
+  // K = [tile L | ... | tile I] (k_zupdate segments).  The decisions use the pending bound
+  // (R21), not a measured maximum, so they are the same as step by step; the contribution of
+  // tile X is scaled by the later steps' decisions inside the contraction.  Every tile uses
+  // nkS_max chunks (a ragged last tile is zero-padded), so the segments are uniform.
+  const int G = std::max(1, std::min(kZMaxG, ctx_fusion()));
   // workspace (stream-ordered)
   const int nkS_max = (nb + kZBK - 1) / kZBK;
   const int n_nt = (n + kZBN - 1) / kZBN;
+  const int NS = 2 * G;   // W / sy / panel sets: two groups (lookahead) of G slots
   const size_t wsz = (size_t)n_nt * 2 * nkS_max * (kZBBytes / 8);   // doubles per W set
   const size_t apk = (size_t)((m + kZBM - 1) / kZBM) * 2 * nkS_max * (kZABytes / 8);   // packed panel
   size_t off[13], tot = 0;
   const size_t sz[13] = {sizeof(int) * n, sizeof(double2) * n, sizeof(double) * n, sizeof(int) * n, sizeof(double) * n,
                          sizeof(int) * (size_t)M * n, sizeof(double) * (size_t)M * n, sizeof(double) * m,
-                         sizeof(double) * m, sizeof(double) * 2 * wsz, sizeof(int) * 4, sizeof(int) * 2 * n,
-                         sizeof(double) * apk};
+                         sizeof(double) * m, sizeof(double) * NS * wsz, sizeof(int) * 4, sizeof(int) * NS * (size_t)n,
+                         sizeof(double) * NS * apk};
   for (int i = 0; i < 13; ++i) { off[i] = tot; tot += align256(sz[i]); }
   ZWork wk;
   ZCK(wk.alloc(tot, st));
@@ -685,14 +756,16 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   }
   int Itop = M - 1;
   while (Itop >= 0 && csI[Itop] == n) --Itop;
-  // Lookahead (DESIGN.md s.6 "Complex pencils"): the update of step I is split into the band
-  // (the rows of tile I-1) and the rest; the solve of tile I-1 runs on a high-priority stream
-  // beside the rest.  The scaling decisions use the pending bound (R21), so the solve needs
-  // nothing from the rest; W and sy alternate between two sets by step parity, so the solve of
-  // tile I-1 never overwrites what the rest of step I's update still reads.
+  // Lookahead (DESIGN.md s.6 "Complex pencils"): the chain of a step group -- its solves, band
+  // updates and the part of the previous group's update that covers its band -- runs on a
+  // high-priority stream; the rest of the previous group's update (the rows above the band)
+  // runs on the caller's stream beside it.  The decisions use the pending bound (R21), so the
+  // chain needs nothing from the rest; W, sy and the packed panels alternate between two sets
+  // of G slots by group, and the chain waits for the rest of the group before last (whose
+  // rows its own band part updates next) before it writes the set that rest reads.
   const bool la = la_mode != 0 && Itop >= 1;   // zz_set_lookahead(0) turns it off
   cudaStream_t hp = nullptr;
-  cudaEvent_t ev_band = nullptr, ev_diag = nullptr;
+  cudaEvent_t ev_dec = nullptr, ev_rest = nullptr;
   struct Guard {
     cudaStream_t& h; cudaEvent_t& a; cudaEvent_t& b; cudaStream_t st;
     ~Guard() {
@@ -702,15 +775,16 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
       if (a) cudaEventDestroy(a);
       if (b) cudaEventDestroy(b);
     }
-  } guard{hp, ev_band, ev_diag, st};
+  } guard{hp, ev_dec, ev_rest, st};
   if (la) {
     int lo, hi;
     ZCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     ZCK(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, hi));
-    ZCK(cudaEventCreateWithFlags(&ev_band, cudaEventDisableTiming));
-    ZCK(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
+    ZCK(cudaEventCreateWithFlags(&ev_dec, cudaEventDisableTiming));
+    ZCK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
   }
-  auto diag = [&](int I, cudaStream_t s) -> cudaError_t {
+  cudaStream_t cs_ = la ? hp : st;   // the chain's stream
+  auto diag = [&](int I, int slot, int zero_begin) -> cudaError_t {
     const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I], n_act = n - cs;
     ZDiagParams p;
     p.I = I; p.r0 = r0; p.nt = nt; p.cs = cs; p.n_act = n_act; p.n_sel = n;
@@ -719,64 +793,101 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.e_pend = d_epend; p.nYb = d_nYb;
     p.e_seg = d_eseg + (size_t)I * n;
     p.nrmh_seg = d_nrmh + (size_t)I * n;
-    p.W = d_W + (size_t)(I & 1) * wsz;
-    p.nkS = (nt + kZBK - 1) / kZBK;
-    p.sy = d_sy + (size_t)(I & 1) * n;
-    const int grid = std::min((n_act + kZWarps - 1) / kZWarps, nsm);   // one 132 KB CTA per SM
-    k_zdiag<<<grid, kZWarps * 32, smem, s>>>(p);
+    p.W = d_W + (size_t)slot * wsz;
+    p.nkS = nkS_max;
+    p.sy = d_sy + (size_t)slot * n;
+    p.zero_begin = std::min(zero_begin, cs);
+    const int zb = (cs - p.zero_begin + kZWarps - 1) / kZWarps;
+    const int grid = std::min(std::max((n_act + kZWarps - 1) / kZWarps, zb), nsm);   // one 132 KB CTA per SM
+    k_zdiag<<<grid, kZWarps * 32, smem, cs_>>>(p);
     ++launches;
     return cudaGetLastError();
   };
-  // the panel of step I in fragment order (rows 0 .. r0 - 1)
-  auto pack = [&](int I) -> cudaError_t {
-    const int r0 = I * nb, nt = std::min(nb, m - r0), nkS = (nt + kZBK - 1) / kZBK;
-    k_zpack<<<dim3((r0 + kZBM - 1) / kZBM, 2 * nkS), 256, 0, st>>>(S, lds, T, ldt, r0, nt, nkS, d_A);
+  // the panel of step I in fragment order (rows 0 .. r0 - 1), into panel slot `slot`
+  auto pack = [&](int I, int slot) -> cudaError_t {
+    const int r0 = I * nb, nt = std::min(nb, m - r0);
+    k_zpack<<<dim3((r0 + kZBM - 1) / kZBM, 2 * nkS_max), 256, 0, cs_>>>(S, lds, T, ldt, r0, nt, nkS_max,
+                                                                       d_A + (size_t)slot * apk);
     ++launches;
     return cudaGetLastError();
   };
-  // Y(row0:row0+rows, cs:n) <- 2^sy Y + [S_panel | T_panel](row0:row0+rows, :) W_I
-  auto update = [&](int I, int row0, int rows) -> cudaError_t {
-    const int r0 = I * nb, nt = std::min(nb, m - r0), cs = csI[I];
+  // Y(row0:row1, cs:n) <- 2^sy Y + sum_e [S_panel | T_panel]_e W_e for the nseg slots from
+  // `slot` (tiles L, L+1, ...; cs = the first column active at tile L)
+  auto update = [&](int L, int slot, int nseg, int row0, int row1, cudaStream_t us) -> cudaError_t {
+    const int cs = csI[L];
     ZUpdParams up;
     up.row_lo = row0;
-    up.rows = row0 + rows;
-    up.nkc = 2 * ((nt + kZBK - 1) / kZBK);
+    up.rows = row1;
+    up.nkc = 2 * nkS_max;
     up.c_begin = cs;
     up.n_sel = n;
     up.ntile0 = cs / kZBN;
     up.mtile0 = row0 / kZBM;
     up.X = X;
     up.ldx = ldx;
-    up.A = d_A;
-    up.W = d_W + (size_t)(I & 1) * wsz;
-    up.sy = d_sy + (size_t)(I & 1) * n;
-    const int n_mt = (row0 + rows - 1) / kZBM - up.mtile0 + 1, n_ntl = n_nt - up.ntile0;
-    if (rows <= 0 || n_ntl <= 0) return cudaSuccess;
+    up.A = d_A + (size_t)slot * apk;
+    up.W = d_W + (size_t)slot * wsz;
+    up.sy = d_sy + (size_t)slot * n;
+    up.nseg = nseg;
+    up.a_stride = (long long)apk;
+    up.w_stride = (long long)wsz;
+    up.sy_stride = n;
+    const int n_mt = (row1 - 1) / kZBM - up.mtile0 + 1, n_ntl = n_nt - up.ntile0;
+    if (row1 <= row0 || n_ntl <= 0) return cudaSuccess;
     // one tile per CTA: CTAs retire after each tile, so the high-priority diagonal solve of the
     // lookahead finds free SMs (measured: a persistent grid of 2 CTAs per SM was slower with it)
-    k_zupdate<<<n_mt * n_ntl, kZUThreads, kZUSmem, st>>>(up, n_mt, n_ntl);
+    k_zupdate<<<n_mt * n_ntl, kZUThreads, kZUSmem, us>>>(up, n_mt, n_ntl);
     ++launches;
     info->update_launches++;
     return cudaGetLastError();
   };
-  if (Itop >= 0) ZCK(diag(Itop, st));
-  for (int I = Itop; I >= 0; --I) {
-    const int r0 = I * nb;
-    if (la && I < Itop) ZCK(cudaStreamWaitEvent(st, ev_diag, 0));
-    if (r0 == 0) break;
-    ZCK(pack(I));
-    if (la) {
-      const int rb = r0 - nb;   // tile I-1 is a full tile
-      ZCK(update(I, rb, nb));
-      ZCK(cudaEventRecord(ev_band, st));
-      ZCK(cudaStreamWaitEvent(hp, ev_band, 0));
-      ZCK(diag(I - 1, hp));
-      ZCK(cudaEventRecord(ev_diag, hp));
-      if (rb > 0) ZCK(update(I, 0, rb));
-    } else {
-      ZCK(update(I, 0, r0));
-      ZCK(diag(I - 1, st));
+  // groups are fixed by the tile index counted from M-1 (not by the selection), so a column's
+  // arithmetic does not depend on which other columns are computed; the last step of a group
+  // needs rows above it (index >= 1)
+  auto group_len = [&](int I) {
+    int len = G - (M - 1 - I) % G;
+    while (len > 1 && I - (len - 1) < 1) --len;
+    return len;
+  };
+  if (la) {   // fork the chain's stream from the caller's
+    ZCK(cudaEventRecord(ev_dec, st));
+    ZCK(cudaStreamWaitEvent(hp, ev_dec, 0));
+  }
+  int gpar = 0;
+  bool rest_pending = false;   // the previous group's rest update runs on st (lookahead)
+  for (int I = Itop; I >= 0;) {
+    if (I == 0) {               // the top rows: solve only
+      ZCK(diag(0, gpar * G, csI[0]));
+      break;
     }
+    const int len = group_len(I), L = I - len + 1, sb = gpar * G;
+    for (int X = I; X >= L; --X) {
+      ZCK(diag(X, sb + (X - L), csI[L]));
+      ZCK(pack(X, sb + (X - L)));
+      if (X > L) ZCK(update(X, sb + (X - L), 1, L * nb, X * nb, cs_));   // the group's band
+    }
+    if (len >= 2) info->fused_pairs++;
+    // the update of all rows above tile L with the group's len segments
+    int rb = 0;                 // lookahead: rows [rb, L nb) are the next group's band
+    if (la && L - 1 >= 1) rb = (L - group_len(L - 1)) * nb;
+    if (la && rest_pending) ZCK(cudaStreamWaitEvent(hp, ev_rest, 0));
+    if (la && rb > 0) {
+      ZCK(update(L, sb, len, rb, L * nb, hp));
+      ZCK(cudaEventRecord(ev_dec, hp));
+      ZCK(cudaStreamWaitEvent(st, ev_dec, 0));
+      ZCK(update(L, sb, len, 0, rb, st));
+      ZCK(cudaEventRecord(ev_rest, st));
+      rest_pending = true;
+    } else {
+      ZCK(update(L, sb, len, 0, L * nb, cs_));
+      rest_pending = false;
+    }
+    gpar ^= la ? 1 : 0;
+    I = L - 1;
+  }
+  if (la) {   // join the chain back into the caller's stream
+    ZCK(cudaEventRecord(ev_dec, hp));
+    ZCK(cudaStreamWaitEvent(st, ev_dec, 0));
   }
   k_znorm<<<n, 256, 0, st>>>(X, ldx, nb, n, d_jcol, d_eseg, d_nrmh, col_scale_exp);
   ++launches;

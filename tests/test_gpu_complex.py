@@ -124,27 +124,56 @@ def test_ztgevc_large_sampled(zz):
     assert np.abs(X[:, cols] - ref["X"]).max() < TOL
 
 
-@pytest.mark.parametrize("z3m", ["0", "1"])
-@pytest.mark.parametrize("la", ["0", "1"])
+def _run_mode(zz, S, T, la, fusion, select=None, tile=64):
+    zz.set_lookahead(la)
+    zz.set_fusion(fusion)
+    try:
+        return _run(zz, S, T, select=select, tile=tile)
+    finally:
+        zz.set_lookahead(1)
+        zz.set_fusion(4)
+
+
+@pytest.mark.parametrize("fusion", [1, 2, 3, 4])
+@pytest.mark.parametrize("la", [0, 1])
 @pytest.mark.parametrize("stress", [False, True])
-def test_ztgevc_lookahead_modes(zz, monkeypatch, la, stress, z3m):
-    """Both schedules (ZZ_ZLOOKAHEAD: the tile solve on a high-priority stream beside the
-    bulk of the previous update, or everything in stream order) against the oracle, on a
-    pencil with selected columns opening mid-wavefront."""
-    monkeypatch.setenv("ZZ_ZLOOKAHEAD", la)
-    monkeypatch.setenv("ZZ_Z3M", z3m)      # ZGEMM or Gauss 3M update (R23)
+def test_ztgevc_lookahead_and_step_groups(zz, la, fusion, stress):
+    """Both schedules (zz_set_lookahead: the chain of a step group on a high-priority stream
+    beside the rest of the previous group's update, or everything in stream order) and step
+    groups of 1-4 tiles (zz_set_fusion: one update with K segments per group) against the
+    oracle, on a pencil with selected columns opening mid-wavefront and mid-group."""
     m = 700
     S, T = gen.complex_pencil(m, seed=12, stress=stress)
     sel = np.ones(m, np.int32)
     sel[600:] = 0            # the top steps have no active columns
     sel[::7] = 0
-    X, e = _run(zz, S, T, select=sel, tile=64)
+    X, e = _run_mode(zz, S, T, la, fusion, select=sel, tile=64)
+    info = zz.last_info()
     ref = oracle.ztgevc(S, T, select=sel)
     assert np.isfinite(X).all()
     big = np.abs(ref["X"]) > 1e-200
     assert np.abs(X[big] - ref["X"][big]).max() < (1e-9 if stress else TOL)
     if stress:
         assert (e < 0).any()
+    assert (info["fused_pairs"] > 0) == (fusion > 1)
+
+
+@pytest.mark.parametrize("fusion", [1, 4])
+def test_ztgevc_schedule_and_select_bitwise(zz, fusion):
+    """The lookahead only reorders launches over disjoint rows, and a column's arithmetic does
+    not depend on which other columns are selected (step groups are fixed by the tile index):
+    bit for bit the same columns (stress pencil: scalings inside the groups)."""
+    m = 640
+    S, T = gen.complex_pencil(m, seed=14, stress=True)
+    X0, e0 = _run_mode(zz, S, T, 0, fusion, tile=64)
+    X1, e1 = _run_mode(zz, S, T, 1, fusion, tile=64)
+    assert np.array_equal(X0, X1) and np.array_equal(e0, e1)
+    assert (e0 < 0).any()
+    sel = np.zeros(m, np.int32)
+    cols = [3, 64, 200, 201, 350, 511, 512, 639]
+    sel[cols] = 1
+    Xs, es = _run_mode(zz, S, T, 1, fusion, select=sel, tile=64)
+    assert np.array_equal(Xs, X0[:, cols]) and np.array_equal(es, e0[cols])
 
 
 def test_ztgevc_padded_leading_dimensions(zz):

@@ -26,15 +26,20 @@ ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--no-check", action="store_true")
 ap.add_argument("--lookahead", type=int, default=1)
+ap.add_argument("--fusion", type=int, default=4)
+ap.add_argument("--lib", default="")   # development: another build of libzz.so (A/B)
 args = ap.parse_args()
 
 m = args.m
 t0 = time.time()
 S, T = gen.complex_pencil(m, seed=args.seed)
 tgen = time.time() - t0
+if args.lib:
+    zz._SO = os.path.abspath(args.lib)
 zz.init(0)
 zz.set_tile(args.tile)
 zz.set_lookahead(args.lookahead)
+zz.set_fusion(args.fusion)
 Sd = torch.from_numpy(S).cuda().t().contiguous().t()
 Td = torch.from_numpy(T).cuda().t().contiguous().t()
 st = torch.cuda.current_stream()
@@ -56,7 +61,7 @@ info = zz.last_info()
 out = {"metric": "seconds & FP64 TFLOP/s, all eigenvectors of a complex Schur pencil (zz_ztgevc)",
        "m": m, "tile": info["mb"], "steps": args.steps, "warmup": args.warmup,
        "seconds_per_call": sec, "flops_nominal": F, "value": F / sec * 1e-12, "unit": "TFLOP/s",
-       "update_product": "gauss3m (k_zupdate, three DMMA contractions)", "lookahead": args.lookahead,
+       "update_product": "gauss3m (k_zupdate, three DMMA contractions)", "lookahead": args.lookahead, "fusion": args.fusion,
        # the Gauss 3M update executes 3/4 of F_z's real flops: the first ratio is an effective
        # (time-to-solution) figure, the second the executed flops' share of the DMMA peak
        "effective_fraction_nominal_flops": F / sec * 1e-12 / 37.0,

@@ -17,6 +17,9 @@ import paper_2003_04776_b200 as zz
 
 VARIANTS = [(128, 4, 1), (128, 6, 1), (96, 4, 1), (96, 6, 1), (64, 4, 1), (64, 6, 1)]
 C2_EXTRA = [(128, 4, 2), (64, 4, 2), (64, 6, 2)]
+if os.environ.get("TF_VARIANTS"):      # e.g. "32:4:1,32:4:2,64:4:1,64:4:2"
+    VARIANTS = [tuple(int(x) for x in v.split(":")) for v in os.environ["TF_VARIANTS"].split(",")]
+    C2_EXTRA = []
 
 
 def main():
