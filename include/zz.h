@@ -154,7 +154,8 @@ int zz_set_timing(int on);
  * how conservative the scaling bounds are (DESIGN.md s.6); groups are fixed by the tile
  * index, so results never depend on `select`.  Tiles of more than 128 rows always run
  * ungrouped.  zz_ztgevc groups min(k, 4) steps (its decisions use the pending bound, so
- * they are those of the ungrouped schedule; results differ by summation order only).
+ * they are those of the ungrouped schedule; results differ by summation order only); until
+ * zz_set_fusion is called it picks 1..4 from the number of tile rows (m / tile + 16) / 32.
  * Returns 0, -1 (k not in 1..6) or -103. */
 int zz_set_fusion(int k);
 
@@ -272,8 +273,8 @@ int zz_tgevc_left(int m, const double* S, int lds, const double* T, int ldt, con
  * most 4 steps) is one complex contraction of K = 2 x tile per step (this library's DMMA
  * kernel, Gauss's three-multiplication form, R23) over fragment-ordered copies of
  * the S and T panels; zz_set_lookahead(0) runs the chain of diagonal solves in line instead
- * of on a high-priority stream (bitwise the same result).  The call
- * allocates its workspace stream-ordered (cudaMallocAsync) and returns after the stream has
+ * of on a high-priority stream (bitwise the same result).  The
+ * workspace is kept by the context between calls; the call returns after the stream has
  * completed.  Status codes as zz_tgevc (-104 non-finite diagonal entry, -107). */
 int zz_ztgevc(int m, const double* S, int lds, const double* T, int ldt, const int* select,
               double* X, int ldx, int* col_scale_exp);

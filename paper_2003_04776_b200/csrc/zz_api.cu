@@ -60,6 +60,8 @@ struct Context {
   int timing = 0;
   // step groups of the wavefront: k consecutive steps share one update (zz_set_fusion)
   int fusion = 4;
+  bool fusion_explicit = false;   // zz_set_fusion was called (zz_ztgevc's default depends on m)
+  Buf zw;                         // zz_ztgevc's workspace (kept between calls)
   // CUDA graph of the wavefront (zz_set_graphs): the last captured plan and its replayable exec
   int graphs = 1;
   cudaGraphExec_t gexec = nullptr;
@@ -101,6 +103,7 @@ struct Context {
     Buf* all[] = {&sub, &colf, &coli, &items, &tiles, &rows, &blks, &state, &seg, &norms, &W,
                   &status, &tmp, &Sc, &Tc, &Xi, &egrp, &hS, &hT, &hX, &hE};
     for (Buf* b : all) b->release();
+    zw.release();
     for (Buf& b : Wx) b.release();
     for (Buf& b : Wy) b.release();
     sYb.release();
@@ -1309,6 +1312,9 @@ int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info) {
 }
 
 int ctx_fusion() { return g_ctx ? g_ctx->fusion : 1; }
+int ctx_fusion_explicit() { return g_ctx && g_ctx->fusion_explicit; }
+// zz_ztgevc's workspace, kept by the context between calls (nullptr: out of memory)
+void* ctx_zwork(size_t bytes) { return (g_ctx && g_ctx->zw.ensure(bytes) == cudaSuccess) ? g_ctx->zw.p : nullptr; }
 
 extern "C" {
 
@@ -1383,6 +1389,7 @@ int zz_set_fusion(int k) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
   if (k < 1 || k > kMaxGroup) return -1;
   g_ctx->fusion = k;
+  g_ctx->fusion_explicit = true;
   return 0;
 }
 

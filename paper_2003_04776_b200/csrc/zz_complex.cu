@@ -27,6 +27,8 @@
 
 int ctx_acquire(cudaStream_t* st, int* mb, int* lookahead, zz_info_t** info);
 int ctx_fusion();
+int ctx_fusion_explicit();
+void* ctx_zwork(size_t bytes);
 
 namespace zz {
 namespace {
@@ -35,16 +37,20 @@ constexpr int kZMaxNB = 64;        // rows per tile: two rows per lane
 // k_zupdate tiling (below)
 constexpr int kZBM = 64;        // complex rows per CTA tile
 constexpr int kZBN = 32;        // columns per CTA tile
-constexpr int kZBK = 8;         // complex panel columns per chunk
-constexpr int kZStages = 5;
-constexpr int kZABytes = 3 * kZBM * kZBK * 8;      // 12 KB: [8 row groups][3 planes][2][32]
-constexpr int kZBBytes = 3 * kZBK * kZBN * 8;      // 6 KB: [3][kZBK/4][32][4]
+constexpr int kZBK = 16;        // complex panel columns per chunk (8 with 5 stages: 82 -> 78 ms at
+                                // m = 10000, the barrier wait amortised over 96 instead of 48 DMMAs)
+constexpr int kZKS = kZBK / 4;  // DMMA k-steps per chunk
+constexpr int kZWPlane = kZBK * kZBN;   // doubles per plane of a W chunk
+constexpr int kZStages = 3;
+constexpr int kZABytes = 3 * kZBM * kZBK * 8;      // 24 KB: [8 row groups][3 planes][kZKS][32]
+constexpr int kZBBytes = 3 * kZBK * kZBN * 8;      // 12 KB: [3][kZKS][32][4]
 constexpr int kZUThreads = 5 * 32;
 constexpr int kZUSmem = kZStages * (kZABytes + kZBBytes) + 2 * kZStages * 8;
 constexpr int kZNGroup = 64;    // N tiles per group of the CTA order
 constexpr int kZMaxG = 4;       // steps per step group (K segments of one update)
 
-constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag
+constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag (16 or 8, leaving room for
+                                   // an update CTA beside it, measured slower: r02ak)
 constexpr int kZErrNonfinite = 0;  // status key = 2*row + kind
 constexpr int kZErrCplxDiag = 1;
 
@@ -63,7 +69,7 @@ struct ZDiagParams {
   int* e_seg;        // row I of the M x n_sel array
   double* nrmh_seg;  // row I
   double* W;         // update operand, k_zupdate's layout [n-tile][chunk][3 planes][2][32][4]
-  int nkS;           // chunks of 8 panel columns per part (S, then T)
+  int nkS;           // chunks of kZBK panel columns per part (S, then T)
   int* sy;           // per column: exponent shift of the pending rows (<= 0), this step's set
   int zero_begin;    // step groups: columns [zero_begin, cs) are not active at this step but
                      // are in the group's fused update -- their W and sy are written as zero
@@ -174,15 +180,15 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
   }
   for (int r = threadIdx.x; r < nt; r += blockDim.x) { cS[r] = p.cmS[r0 + r]; cT[r] = p.cmT[r0 + r]; }
   if (p.zero_begin < p.cs) {
-    const int per = 16 * p.nkS;   // W rows (S part, then T part) of a column
+    const int per = 2 * kZBK * p.nkS;   // W rows (S part, then T part) of a column
     const long long nz = (long long)(p.cs - p.zero_begin) * per;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nz; q += (long long)gridDim.x * blockDim.x) {
       const int c = p.zero_begin + (int)(q / per), kk = (int)(q % per);
       double* o = p.W + (long long)(c / kZBN) * (2 * p.nkS) * (kZBBytes / 8) + (c % kZBN) * 4 +
                   (long long)(kk / kZBK) * (kZBBytes / 8) + ((kk % kZBK) >> 2) * (kZBN * 4) + (kk & 3);
       o[0] = 0.0;
-      o[256] = 0.0;
-      o[512] = 0.0;
+      o[kZWPlane] = 0.0;
+      o[2 * kZWPlane] = 0.0;
       if (kk == 0) p.sy[c] = 0;
     }
   }
@@ -276,7 +282,9 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
       // y_l <- y_l - S_li u + T_li v as 8 fused multiply-adds per row (the oracle rounds each
       // product: results agree to rounding, R22)
       if (lane < i) y0 = zaxpy2(y0, Ss[i * nt + lane], u, Ts[i * nt + lane], v);
-      if (lane + 32 < i) y1 = zaxpy2(y1, Ss[i * nt + lane + 32], u, Ts[i * nt + lane + 32], v);
+      if (i > 32) {   // warp-uniform: the lanes' second rows are pending only above row 32
+        if (lane + 32 < i) y1 = zaxpy2(y1, Ss[i * nt + lane + 32], u, Ts[i * nt + lane + 32], v);
+      }
       bw = bw + tb * ax;
     }
     if (lane <= top) xc[lane] = y0;
@@ -328,18 +336,18 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int row = lane + 32 * h;
-      if (row >= 8 * p.nkS) continue;
+      if (row >= kZBK * p.nkS) continue;
       const bool z = row > top;
       const double2 ws = z ? make_double2(0.0, 0.0) : make_double2(-(be * xs[h].x), -(be * xs[h].y));
       const double2 wt = z ? make_double2(0.0, 0.0) : zmul(al, xs[h]);
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
-        const int kk = part ? 8 * p.nkS + row : row;
+        const int kk = part ? kZBK * p.nkS + row : row;
         const double2 w = part ? wt : ws;
         double* o = Wt + (long long)(kk / kZBK) * (kZBBytes / 8) + ((kk % kZBK) >> 2) * (kZBN * 4) + (kk & 3);
         o[0] = w.x;
-        o[256] = w.y;
-        o[512] = __dadd_rn(w.x, w.y);
+        o[kZWPlane] = w.y;
+        o[2 * kZWPlane] = __dadd_rn(w.x, w.y);
       }
     }
   }
@@ -361,18 +369,18 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
 // in k_zdiag is ProtectUpdate(2 y^, 4 sums, x^).
 //
 // k_zpack writes the panel of the step once in DMMA fragment order with its three planes
-// ([64-row tile][chunk of 8 columns][8-row group][plane][k/4][lane]), so that a stage is one
-// 12 KB bulk copy and every fragment load is one conflict-free 8-byte shared load (a TMA copy
+// ([64-row tile][chunk of 16 columns][8-row group][plane][k/4][lane]), so that a stage is one
+// 24 KB bulk copy and every fragment load is one conflict-free 8-byte shared load (a TMA copy
 // of the interleaved column-major panel gives 4-way conflicts on the 16-byte (Re, Im) loads).
 // Pipeline as the real update (zz_update.cu): CTA tile 64 complex rows x 32 columns (aligned
 // 64-row tiles from row 0; rows outside [row_lo, rows) are computed but not stored), four DMMA
-// warps (32 rows x 16 columns each) and one producer warp, per stage 8 panel columns (12 KB)
-// and the matching 6 KB of W.  The contraction is computed transposed (Y^T += W^T A^T): a
+// warps (32 rows x 16 columns each) and one producer warp, per stage 16 panel columns (24 KB)
+// and the matching 12 KB of W, a 3-stage mbarrier ring.  The contraction is computed transposed (Y^T += W^T A^T): a
 // lane's accumulators are two consecutive complex rows of one column (32-byte loads/stores).
 // ------------------------------------------------------------------------------------
 struct ZUpdParams {
   int rows, row_lo;   // complex rows [row_lo, rows) are updated
-  int nkc;            // chunks of 8 panel columns (S part, then T part)
+  int nkc;            // chunks of kZBK panel columns (S part, then T part)
   int c_begin, n_sel; // active columns
   int ntile0;         // first 32-column tile (c_begin / 32)
   int mtile0;         // first 64-row tile (row_lo / 64)
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(256) k_zpack(const double2* __restrict__ S, lo
   __syncthreads();
   double* out = A + ((long long)mt * gridDim.y + kc) * (kZABytes / 8);
   for (int o = threadIdx.x; o < kZABytes / 8; o += blockDim.x) {
-    const int ln = o & 31, ks = (o >> 5) & 1, pl = (o >> 6) % 3, g = (o >> 6) / 3;
+    const int ln = o & 31, ks = (o >> 5) % kZKS, pl = ((o >> 5) / kZKS) % 3, g = (o >> 5) / (3 * kZKS);
     const double2 v = tile[ks * 4 + (ln & 3)][g * 8 + (ln >> 2)];
     out[o] = pl == 0 ? v.x : (pl == 1 ? v.y : __dadd_rn(v.x, v.y));
   }
@@ -529,8 +537,8 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
     _Pragma("unroll") for (int ni = 0; ni < 2; ++ni) {                               \
       const int o = (ks * kZBN + wn * 16 + ni * 8 + cq) * 4 + rq;                    \
       wr[ni] = b[o];                                                                 \
-      wi[ni] = b[256 + o];                                                           \
-      ws[ni] = b[512 + o];                                                           \
+      wi[ni] = b[kZWPlane + o];                                                      \
+      ws[ni] = b[2 * kZWPlane + o];                                                  \
       if (SCALE) {                                                                   \
         wr[ni] = ldexp(wr[ni], sc[ni]);                                              \
         wi[ni] = ldexp(wi[ni], sc[ni]);                                              \
@@ -539,9 +547,9 @@ __global__ void __launch_bounds__(kZUThreads, 2) k_zupdate(ZUpdParams p, int n_m
     }                                                                                \
     _Pragma("unroll") for (int mi = 0; mi < 4; ++mi) {                               \
       const int g = wm * 4 + mi;                                                     \
-      fr[mi] = a[((g * 3 + 0) * 2 + ks) * 32 + lane];                                \
-      fi[mi] = a[((g * 3 + 1) * 2 + ks) * 32 + lane];                                \
-      fs[mi] = a[((g * 3 + 2) * 2 + ks) * 32 + lane];                                \
+      fr[mi] = a[((g * 3 + 0) * kZKS + ks) * 32 + lane];                                \
+      fi[mi] = a[((g * 3 + 1) * kZKS + ks) * 32 + lane];                                \
+      fs[mi] = a[((g * 3 + 2) * kZKS + ks) * 32 + lane];                                \
     }                                                                                \
     _Pragma("unroll") for (int ni = 0; ni < 2; ++ni)                                 \
       _Pragma("unroll") for (int mi = 0; mi < 4; ++mi) {                             \
@@ -620,20 +628,6 @@ __global__ void __launch_bounds__(256) k_znorm(double2* X, long long ldx, int nb
   }
 }
 
-struct ZWork {
-  void* p = nullptr;
-  size_t n = 0;
-  cudaStream_t st = nullptr;
-  cudaError_t alloc(size_t bytes, cudaStream_t s) {
-    st = s;
-    n = bytes;
-    return cudaMallocAsync(&p, bytes, s);
-  }
-  ~ZWork() {
-    if (p) cudaFreeAsync(p, st);
-  }
-};
-
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
@@ -691,7 +685,11 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   // (R21), not a measured maximum, so they are the same as step by step; the contribution of
   // tile X is scaled by the later steps' decisions inside the contraction.  Every tile uses
   // nkS_max chunks (a ragged last tile is zero-padded), so the segments are uniform.
-  const int G = std::max(1, std::min(kZMaxG, ctx_fusion()));
+  // Default group length by the number of steps (measured, profiles/r02ak_zab.txt: m = 2000 is
+  // fastest ungrouped, 4000 in pairs, 6000 in triples, 10000 in groups of 3-4: short wavefronts
+  // are bound by the chain, which the group's band updates lengthen); zz_set_fusion overrides.
+  const int G = ctx_fusion_explicit() ? std::max(1, std::min(kZMaxG, ctx_fusion()))
+                                      : std::max(1, std::min(kZMaxG, (M + 16) / 32));
   // workspace (stream-ordered)
   const int nkS_max = (nb + kZBK - 1) / kZBK;
   const int n_nt = (n + kZBN - 1) / kZBN;
@@ -704,9 +702,10 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
                          sizeof(double) * m, sizeof(double) * NS * wsz, sizeof(int) * 4, sizeof(int) * NS * (size_t)n,
                          sizeof(double) * NS * apk};
   for (int i = 0; i < 13; ++i) { off[i] = tot; tot += align256(sz[i]); }
-  ZWork wk;
-  ZCK(wk.alloc(tot, st));
-  char* base = static_cast<char*>(wk.p);
+  // kept by the context between calls (a stream-ordered allocation returned its memory to the
+  // driver at every call's final synchronisation: sporadic calls 10-15 ms longer at m = 10000)
+  char* base = static_cast<char*>(ctx_zwork(tot));
+  if (!base) return ZZ_ERR_NOMEM;
   int* d_jcol = reinterpret_cast<int*>(base + off[0]);
   double2* d_alpha = reinterpret_cast<double2*>(base + off[1]);
   double* d_beta = reinterpret_cast<double*>(base + off[2]);
@@ -770,7 +769,7 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     cudaStream_t& h; cudaEvent_t& a; cudaEvent_t& b; cudaStream_t st;
     ~Guard() {
       // on every exit (errors included) the work queued on the high-priority stream has
-      // finished before the workspace is released on st (ZWork, stream-ordered)
+      // finished before the call returns (the context's workspace is reused by the next call)
       if (h) { cudaStreamSynchronize(h); cudaStreamDestroy(h); }
       if (a) cudaEventDestroy(a);
       if (b) cudaEventDestroy(b);
