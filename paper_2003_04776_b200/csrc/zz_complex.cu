@@ -2,7 +2,7 @@
 // form (the ZTGEVC analogue; PAPER.md:333 names complex pencils as the next step, SURVEY.md
 // s.8(f) NEXT-4).  Every diagonal block is 1x1, so the method is Algorithm 1
 // with complex entries: a wavefront over tiles I = M-1 .. 0 of
-//   (2) a robust diagonal-tile solve per active eigenvector (k_zdiag, one warp per column,
+//   (2) a robust diagonal-tile solve per active eigenvector (k_zdiag, two or four columns per warp,
 //       the tile of S and T in shared memory, ProtectDivision / ProtectUpdate per row,
 //       PAPER.md:175-200), which also takes the per-column scaling decision of Algorithm 3
 //        and stages the scaled B operand [beta x ; -alpha x];
@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <utility>
 #include <vector>
 
 #include "../../include/zz.h"
@@ -49,8 +50,7 @@ constexpr int kZUSmem = kZStages * (kZABytes + kZBBytes) + 2 * kZStages * 8;
 constexpr int kZNGroup = 64;    // N tiles per group of the CTA order
 constexpr int kZMaxG = 4;       // steps per step group (K segments of one update)
 
-constexpr int kZWarps = 32;        // columns (warps) per CTA of k_zdiag (16 or 8, leaving room for
-                                   // an update CTA beside it, measured slower: r02ak)
+constexpr int kZWarps = 16;        // warps per CTA of k_zdiag (2 or 4 columns per warp)
 constexpr int kZErrNonfinite = 0;  // status key = 2*row + kind
 constexpr int kZErrCplxDiag = 1;
 
@@ -108,10 +108,11 @@ __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+
+// f(R-1), ..., f(0) with the index as a compile-time constant
+template <class F, int... I>
+__device__ __forceinline__ void zfor_rev(std::integer_sequence<int, I...>, F&& f) {
+  (f(std::integral_constant<int, (int)sizeof...(I) - 1 - I>{}), ...);
 }
 
 // Per output column: normalised eigenvalue (R18) and zeroed state; per diagonal entry: the
@@ -164,9 +165,17 @@ __global__ void k_zcolmax(const double2* __restrict__ S, long long lds, const do
 }
 
 // Robust diagonal-tile solve + Algorithm 3's decision
-// + the B operand of the update.  One warp per active column; lane l
-// owns tile rows l and l + 32.
+// + the B operand of the update.  A warp solves C active columns: the
+// L = 32 / C lanes of a column own the tile rows sub + L h (h < R = 64 / L).  The tile is
+// walked bottom-up one row at a time for all C columns together, so the per-row instructions
+// that are the same for every lane of a column (broadcasts, the update bound, Algorithm 2/3's
+// tests, x D and x B) are issued once for C columns; the rows of a column are in registers
+// with static indices (the row loop is unrolled over h, so row i = h L + s updates the
+// register rows h' < h of every lane and row h of the lanes sub < s).  Every column sees
+// exactly the operations of the one-column-per-warp form (bitwise the same results).
+template <int C>
 __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
+  constexpr int L = 32 / C, R = kZMaxNB / L;
   extern __shared__ double2 sm[];
   double2* Ss = sm;                       // nt x nt, column-major
   double2* Ts = sm + p.nt * p.nt;
@@ -194,30 +203,48 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const int sub = lane % L, grp = lane / L;
+  const unsigned gmask = (L == 32 ? 0xffffffffu : ((1u << L) - 1u)) << (grp * L);   // the column's lanes
+  auto gmax = [&](double v) {
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(gmask, v, o));
+    return v;
+  };
+  auto gsum = [&](double v) {
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    return v;
+  };
+  const int ntask = (p.n_act + C - 1) / C;
   const int nw = gridDim.x * kZWarps;
-  for (int w = blockIdx.x * kZWarps + (threadIdx.x >> 5); w < p.n_act; w += nw) {
-    const int c = p.cs + w;
+  for (int w = blockIdx.x * kZWarps + (threadIdx.x >> 5); w < ntask; w += nw) {
+    const bool cv = w * C + grp < p.n_act;       // this group has a column
+    const int c = p.cs + (cv ? w * C + grp : 0);
     const int jl = p.jcol[c] - r0;               // >= nt: not a tip
     const bool tipc = jl < nt;
-    const int top = tipc ? jl : nt - 1;
+    const int top = cv ? (tipc ? jl : nt - 1) : -1;
     const double2 al = p.alpha[c];
     const double be = p.beta[c];
     const double aa = fabs(al.x) + fabs(al.y);
     double2* xc = p.X + (long long)c * p.ldx + r0;
-    double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
-    if (!tipc) {
-      if (lane <= top) y0 = xc[lane];
-      if (lane + 32 <= top) y1 = xc[lane + 32];
+    double2 y[R];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      y[h] = make_double2(0.0, 0.0);
+      if (!tipc && sub + L * h <= top) y[h] = xc[sub + L * h];
     }
-    int e = tipc ? 0 : p.e_pend[c];
-    // Off the dependent chain: the pivots of the lane's two rows (R20) and their reciprocals
+    int e = (tipc || !cv) ? 0 : p.e_pend[c];
+    // Off the dependent chain: the pivots of the lane's rows (R20) and their reciprocals
     // (Smith's formula for 1/d), the ProtectDivision thresholds, and the bound bw >= max |y|
     // over the pending in-tile rows (exact at the start).
-    double2 inv0 = make_double2(0.0, 0.0), inv1 = inv0;
-    double td0 = 1.0, td1 = 1.0;
+    double2 inv[R];
+    double td[R];
+    double bw = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = lane + 32 * h;
+    for (int h = 0; h < R; ++h) {
+      const int r = sub + L * h;
+      inv[h] = make_double2(0.0, 0.0);
+      td[h] = 1.0;
       if (r <= top) {
         const double2 s = Ss[r * nt + r];
         const double t = Ts[r * nt + r].x;
@@ -225,93 +252,96 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
                                  __dsub_rn(__dmul_rn(be, s.y), __dmul_rn(al.y, t)));
         const double smin = fmax(kU * (be * zabs1(s) + aa * fabs(t)), kSmlnum);
         if (zabs1(d) < smin) d = make_double2(smin, 0.0);
-        const double2 iv = zdiv(make_double2(1.0, 0.0), d);
-        const double td = 0.5 * fmin(1.0, zabsm(d));
-        if (h == 0) { inv0 = iv; td0 = td; } else { inv1 = iv; td1 = td; }
+        inv[h] = zdiv(make_double2(1.0, 0.0), d);
+        td[h] = 0.5 * fmin(1.0, zabsm(d));
       }
+      bw = fmax(bw, zabsm(y[h]));
     }
-    double bw = warp_max(fmax(zabsm(y0), zabsm(y1)));
-    for (int i = top; i >= 0; --i) {
-      const int own = i & 31;
-      const bool hi = i >= 32;
-      double2 xi;
-      if (tipc && i == jl) {
-        xi = make_double2(1.0, 0.0);
-        if (lane == own) { if (hi) y1 = xi; else y0 = xi; }
-      } else {
-        // ProtectDivision in the owner lane, then x_i = y_i * (1/d_i)
+    bw = gmax(bw);
+    const int itop = __reduce_max_sync(0xffffffffu, top);   // warp-uniform first row
+    // the rows h L + s, s = L-1 .. 0, of register row h (h a compile-time constant, so that
+    // every register row has a static index)
+    auto rowblock = [&](auto hc) {
+      constexpr int h = decltype(hc)::value;
+      for (int s = min(L - 1, itop - h * L); s >= 0; --s) {
+        const int i = h * L + s;
+        const bool act = i <= top;
+        const bool own = act && sub == s;
+        // the tip's own row is 1 (R18); else ProtectDivision in the owner
+        // lane, then x_i = y_i * (1/d_i)
+        const bool tiprow = tipc && i == jl;
         int k = 0;
-        if (lane == own) k = protect_division(zabsm(hi ? y1 : y0), hi ? td1 : td0);
-        k = __shfl_sync(0xffffffffu, k, own);
+        if (own && !tiprow) k = protect_division(zabsm(y[h]), td[h]);
+        k = __shfl_sync(0xffffffffu, k, s, L);
         if (k < 0) {
-          y0 = zldexp(y0, k);
-          y1 = zldexp(y1, k);
+#pragma unroll
+          for (int q = 0; q < R; ++q) y[q] = zldexp(y[q], k);
           bw = ldexp(bw, k);
           e += k;
         }
-        if (lane == own) {
-          if (hi) y1 = zmul(y1, inv1); else y0 = zmul(y0, inv0);
+        if (own) y[h] = tiprow ? make_double2(1.0, 0.0) : zmul(y[h], inv[h]);
+        double2 xi = make_double2(__shfl_sync(0xffffffffu, y[h].x, s, L), __shfl_sync(0xffffffffu, y[h].y, s, L));
+        if (i == 0) break;   // h = 0, s = 0: the last row
+        // ProtectUpdate of the in-tile rows above (R19 bound).  The bound bw
+        // decides first; only when it cannot exclude a scaling is the exact maximum reduced,
+        // so the decision is the one the exact maximum gives.
+        const double tb = 2.0 * (be * cS[i] + aa * cT[i]);
+        double ax = zabsm(xi);
+        if (act && protect_update(bw, tb, ax) < 0) {
+          double wm = 0.0;
+#pragma unroll
+          for (int q = 0; q < R; ++q)
+            if (q < h || (q == h && sub < s)) wm = fmax(wm, zabsm(y[q]));
+          wm = gmax(wm);
+          const int k2 = protect_update(wm, tb, ax);
+          if (k2 < 0) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) y[q] = zldexp(y[q], k2);
+            xi = zldexp(xi, k2);
+            wm = ldexp(wm, k2);
+            ax = zabsm(xi);
+            e += k2;
+          }
+          bw = wm;
         }
-        const double2 xo = hi ? y1 : y0;
-        xi = make_double2(__shfl_sync(0xffffffffu, xo.x, own), __shfl_sync(0xffffffffu, xo.y, own));
-      }
-      if (i == 0) break;
-      // ProtectUpdate of the in-tile rows above (R19 bound).  The bound bw
-      // decides first; only when it cannot exclude a scaling is the exact maximum reduced,
-      // so the decision is the one the exact maximum gives.
-      const double tb = 2.0 * (be * cS[i] + aa * cT[i]);
-      double ax = zabsm(xi);
-      if (protect_update(bw, tb, ax) < 0) {
-        double wm = 0.0;
-        if (lane < i) wm = zabsm(y0);
-        if (lane + 32 < i) wm = fmax(wm, zabsm(y1));
-        wm = warp_max(wm);
-        const int k2 = protect_update(wm, tb, ax);
-        if (k2 < 0) {
-          y0 = zldexp(y0, k2);
-          y1 = zldexp(y1, k2);
-          xi = zldexp(xi, k2);
-          wm = ldexp(wm, k2);
-          ax = zabsm(xi);
-          e += k2;
+        const double2 u = make_double2(be * xi.x, be * xi.y);   // x D
+        const double2 v = zmul(al, xi);                          // x B
+        // y_l <- y_l - S_li u + T_li v as 8 fused multiply-adds per row (the oracle rounds each
+        // product: results agree to rounding, R22)
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            if (q < h) y[q] = zaxpy2(y[q], Ss[i * nt + sub + L * q], u, Ts[i * nt + sub + L * q], v);
+          }
+          if (sub < s) y[h] = zaxpy2(y[h], Ss[i * nt + sub + L * h], u, Ts[i * nt + sub + L * h], v);
         }
-        bw = wm;
+        if (act) bw = bw + tb * ax;
       }
-      const double2 u = make_double2(be * xi.x, be * xi.y);   // x D
-      const double2 v = zmul(al, xi);                          // x B
-      // y_l <- y_l - S_li u + T_li v as 8 fused multiply-adds per row (the oracle rounds each
-      // product: results agree to rounding, R22)
-      if (lane < i) y0 = zaxpy2(y0, Ss[i * nt + lane], u, Ts[i * nt + lane], v);
-      if (i > 32) {   // warp-uniform: the lanes' second rows are pending only above row 32
-        if (lane + 32 < i) y1 = zaxpy2(y1, Ss[i * nt + lane + 32], u, Ts[i * nt + lane + 32], v);
+    };
+    zfor_rev(std::make_integer_sequence<int, R>{}, rowblock);
+    double nx = 0.0, hh = 0.0, sums = 0.0;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int r = sub + L * h;
+      if (r <= top) {
+        xc[r] = y[h];
+        nx = fmax(nx, zabsm(y[h]));
+        hh = fmax(hh, 0.5 * fabs(y[h].x) + 0.5 * fabs(y[h].y));
+        sums += be * cS[r] + aa * cT[r];
       }
-      bw = bw + tb * ax;
     }
-    if (lane <= top) xc[lane] = y0;
-    if (lane + 32 <= top) xc[lane + 32] = y1;
-    double nx = 0.0, h = 0.0, sums = 0.0;
-    if (lane <= top) {
-      nx = zabsm(y0);
-      h = 0.5 * fabs(y0.x) + 0.5 * fabs(y0.y);
-      sums = be * cS[lane] + aa * cT[lane];
-    }
-    if (lane + 32 <= top) {
-      nx = fmax(nx, zabsm(y1));
-      h = fmax(h, 0.5 * fabs(y1.x) + 0.5 * fabs(y1.y));
-      sums += be * cS[lane + 32] + aa * cT[lane + 32];
-    }
-    nx = warp_max(nx);
-    h = warp_max(h);
-    sums = warp_sum(sums);
-    if (lane == 0) {
+    nx = gmax(nx);
+    hh = gmax(hh);
+    sums = gsum(sums);
+    if (cv && sub == 0) {
       p.e_seg[c] = e;
-      p.nrmh_seg[c] = h;
+      p.nrmh_seg[c] = hh;
     }
     if (r0 == 0) continue;
     // Algorithm 3: one exponent for the pending rows after the update
-    const int ep = tipc ? 0 : p.e_pend[c];
+    const int ep = (tipc || !cv) ? 0 : p.e_pend[c];
     const int g = min(ep, e);
-    const double yh = ldexp(tipc ? 0.0 : p.nYb[c], g - ep);
+    const double yh = ldexp((tipc || !cv) ? 0.0 : p.nYb[c], g - ep);
     const double xh = ldexp(nx, g - e);
     // R23 (k_zupdate): the partial sums of Im + Re accumulate from 2^sy (|Im Y| + |Re Y|) <=
     // 2 y^ and add up to sum_k (|Ar|+|Ai|)(|Wr|+|Wi|) <= 4 sums x^: ProtectUpdate(2 y^, 4 sums, x^)
@@ -320,26 +350,27 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     const int en = g + ed;
     const int sy = en - ep, sx = en - e;
     __syncwarp();
-    if (lane == 0) {
+    if (cv && sub == 0) {
       p.e_pend[c] = en;
       // R21: the bound 2^ed (yh + tau xh), not a measurement; tau xh itself may exceed the
       // range when ed < 0, so that product is formed as protect_update does (scaled by 2^-1023)
-        const double bnd = ed == 0 ? yh + tau * xh
+      const double bnd = ed == 0 ? yh + tau * xh
                                  : ldexp(yh, ed) + ldexp(ldexp(tau, -512) * ldexp(xh, -511), ed + 1023);
       p.nYb[c] = bnd * (1.0 + 0x1p-40);
+      p.sy[c] = sy;   // applied to the pending rows in k_zupdate's prologue
     }
-    if (lane == 0) p.sy[c] = sy;   // applied to the pending rows in k_zupdate's prologue
+    if (!cv) continue;
     // W(:, c) = [-sigma beta x ; sigma alpha x] in k_zupdate's stage layout, planes Re, Im and
     // Re + Im; rows past the tile (or past a tip) are zero
-    const double2 xs[2] = {zldexp(y0, sx), zldexp(y1, sx)};
     double* Wt = p.W + (long long)(c / kZBN) * (2 * p.nkS) * (kZBBytes / 8) + (c % kZBN) * 4;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = lane + 32 * h;
+    for (int h = 0; h < R; ++h) {
+      const int row = sub + L * h;
       if (row >= kZBK * p.nkS) continue;
       const bool z = row > top;
-      const double2 ws = z ? make_double2(0.0, 0.0) : make_double2(-(be * xs[h].x), -(be * xs[h].y));
-      const double2 wt = z ? make_double2(0.0, 0.0) : zmul(al, xs[h]);
+      const double2 xs = zldexp(y[h], sx);
+      const double2 ws = z ? make_double2(0.0, 0.0) : make_double2(-(be * xs.x), -(be * xs.y));
+      const double2 wt = z ? make_double2(0.0, 0.0) : zmul(al, xs);
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         const int kk = part ? kZBK * p.nkS + row : row;
@@ -734,7 +765,8 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
   ZCK(cudaStreamSynchronize(st));
   if (hstatus != big) return (hstatus & 1) == kZErrCplxDiag ? ZZ_ERR_CPLXDIAG : ZZ_ERR_NONFINITE;
   const size_t smem = sizeof(double2) * 2 * nb * nb + sizeof(double) * 2 * kZMaxNB;
-  ZCK(cudaFuncSetAttribute(k_zdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ZCK(cudaFuncSetAttribute(k_zdiag<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ZCK(cudaFuncSetAttribute(k_zdiag<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ZCK(cudaFuncSetAttribute(k_zupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, kZUSmem));
   ZCK(cudaFuncSetAttribute(k_zupdate, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int nsm = 148;
@@ -797,8 +829,14 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     p.sy = d_sy + (size_t)slot * n;
     p.zero_begin = std::min(zero_begin, cs);
     const int zb = (cs - p.zero_begin + kZWarps - 1) / kZWarps;
-    const int grid = std::min(std::max((n_act + kZWarps - 1) / kZWarps, zb), nsm);   // one 132 KB CTA per SM
-    k_zdiag<<<grid, kZWarps * 32, smem, cs_>>>(p);
+    // Two columns per warp while one pass of one CTA per SM covers the step, four beyond
+    // (measured, profiles/r02am_zdiag_ab.txt: m = 2000 2.91 -> 2.43 ms with two, 2.75 with four;
+    // m = 10000 77.0 -> 74.3 with two, 72.3 with four; bitwise the one-column kernel's results)
+    const int cpw = n_act > nsm * kZWarps * 2 ? 4 : 2;
+    const int ntask = (n_act + cpw - 1) / cpw;   // warp tasks
+    const int grid = std::max(1, std::min(std::max((ntask + kZWarps - 1) / kZWarps, zb), nsm));   // one 132 KB CTA per SM
+    if (cpw == 4) k_zdiag<4><<<grid, kZWarps * 32, smem, cs_>>>(p);
+    else k_zdiag<2><<<grid, kZWarps * 32, smem, cs_>>>(p);
     ++launches;
     return cudaGetLastError();
   };

@@ -26,7 +26,7 @@ ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--no-check", action="store_true")
 ap.add_argument("--lookahead", type=int, default=1)
-ap.add_argument("--fusion", type=int, default=4)
+ap.add_argument("--fusion", type=int, default=0)   # 0: the library default (by the number of tile rows)
 ap.add_argument("--lib", default="")   # development: another build of libzz.so (A/B)
 args = ap.parse_args()
 
@@ -39,7 +39,8 @@ if args.lib:
 zz.init(0)
 zz.set_tile(args.tile)
 zz.set_lookahead(args.lookahead)
-zz.set_fusion(args.fusion)
+if args.fusion:
+    zz.set_fusion(args.fusion)
 Sd = torch.from_numpy(S).cuda().t().contiguous().t()
 Td = torch.from_numpy(T).cuda().t().contiguous().t()
 st = torch.cuda.current_stream()
