@@ -156,7 +156,8 @@ int zz_set_timing(int on);
  * ungrouped.  zz_ztgevc groups min(k, 4) steps (its decisions use the pending bound, so
  * they are those of the ungrouped schedule; results differ by summation order only); until
  * zz_set_fusion is called it picks 1..4 from the number of tile rows (m / tile + 16) / 32.
- * Returns 0, -1 (k not in 1..6) or -103. */
+ * k = 0 restores the defaults (4; zz_ztgevc by the number of tile rows).
+ * Returns 0, -1 (k not in 0..6) or -103. */
 int zz_set_fusion(int k);
 
 /* Lookahead schedule: the chain of diagonal solves of a step group runs on a high-priority

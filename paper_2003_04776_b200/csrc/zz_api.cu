@@ -1387,9 +1387,9 @@ int zz_set_tile(int mb) {
 
 int zz_set_fusion(int k) {
   if (!g_ctx) return ZZ_ERR_NOCTX;
-  if (k < 1 || k > kMaxGroup) return -1;
-  g_ctx->fusion = k;
-  g_ctx->fusion_explicit = true;
+  if (k < 0 || k > kMaxGroup) return -1;
+  g_ctx->fusion = k ? k : 4;          // 0: the library defaults
+  g_ctx->fusion_explicit = k != 0;
   return 0;
 }
 

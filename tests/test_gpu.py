@@ -167,9 +167,10 @@ def test_error_codes(zz):
 
 def test_set_fusion_arguments(zz):
     lib = zz.load()
-    assert lib.zz_set_fusion(0) == -1 and lib.zz_set_fusion(7) == -1
+    assert lib.zz_set_fusion(-1) == -1 and lib.zz_set_fusion(7) == -1 and lib.zz_set_fusion(0) == 0
     for k in (1, 6, 4):
         assert lib.zz_set_fusion(k) == 0
+    assert lib.zz_set_fusion(0) == 0   # back to the library defaults
 
 
 def test_select_subsets_bitwise(zz):

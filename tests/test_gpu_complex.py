@@ -111,13 +111,15 @@ def test_ztgevc_status(zz):
     assert X.shape == (0, 0)
 
 
-def test_ztgevc_large_sampled(zz):
-    """m = 4000 in the bench launch configuration (tile 64): sampled columns against the
-    oracle's selected-column solve."""
-    m = 4000
+@pytest.mark.parametrize("m", [4000, 6000])
+def test_ztgevc_large_sampled(zz, m):
+    """m = 4000 and 6000 in the bench launch configuration (tile 64, the library's default
+    step groups): sampled columns against the oracle's selected-column solve.  At m = 6000
+    the steps with more than 148 x 32 active columns run k_zdiag with four columns per warp,
+    the others with two."""
     S, T = gen.complex_pencil(m, seed=10)
     X, _ = _run(zz, S, T)
-    cols = [0, 1, 999, 2047, 2048, 3071, 3998, 3999]
+    cols = [0, 1, 999, 2047, 2048, 3071, m // 2 + 5, m - 1003, m - 2, m - 1]
     sel = np.zeros(m, np.int32)
     sel[cols] = 1
     ref = oracle.ztgevc(S, T, select=sel)
@@ -131,7 +133,7 @@ def _run_mode(zz, S, T, la, fusion, select=None, tile=64):
         return _run(zz, S, T, select=select, tile=tile)
     finally:
         zz.set_lookahead(1)
-        zz.set_fusion(4)
+        zz.set_fusion(0)
 
 
 @pytest.mark.parametrize("fusion", [1, 2, 3, 4])

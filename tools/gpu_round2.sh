@@ -36,3 +36,13 @@ if [ "${SAN:-0}" = "1" ]; then
     timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > $OUT/${TAG}_san_$tool.log 2>&1; echo "sanitizer $tool exit $?"; tail -3 $OUT/${TAG}_san_$tool.log
   done
 fi
+if [ "${COMPLEX:-1}" = "1" ]; then
+  for M in 2000 4000 10000; do
+    timeout 600 python tools/bench_complex.py --m $M > $OUT/${TAG}_complex_$M.json 2> /dev/null
+    python -c "import json; d=json.load(open('$OUT/${TAG}_complex_$M.json')); print('complex m=$M', round(d['seconds_per_call']*1e3,2), 'ms', d.get('parity_sample',{}).get('max_abs'))"
+  done
+  CMDZ="python tools/bench_complex.py --m 10000 --steps 1 --warmup 0 --no-check"
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_complex_launches.csv $CMDZ > /dev/null 2>&1; echo "ncu complex launches exit $?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_zupdate -s 104 -c 1 -o $OUT/${TAG}_zupdate $CMDZ > /dev/null 2>&1; echo "ncu zupdate exit $?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_zdiag -s 120 -c 1 -o $OUT/${TAG}_zdiag $CMDZ > /dev/null 2>&1; echo "ncu zdiag exit $?"
+fi
