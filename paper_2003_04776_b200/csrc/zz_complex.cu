@@ -73,6 +73,7 @@ struct ZDiagParams {
   int* sy;           // per column: exponent shift of the pending rows (<= 0), this step's set
   int zero_begin;    // step groups: columns [zero_begin, cs) are not active at this step but
                      // are in the group's fused update -- their W and sy are written as zero
+  int wact;          // warps of a CTA that solve (all kZWarps stage the tile)
 };
 
 __device__ __forceinline__ double zabsm(double2 z) { return fmax(fabs(z.x), fabs(z.y)); }
@@ -216,8 +217,12 @@ __global__ void __launch_bounds__(kZWarps * 32) k_zdiag(ZDiagParams p) {
     return v;
   };
   const int ntask = (p.n_act + C - 1) / C;
-  const int nw = gridDim.x * kZWarps;
-  for (int w = blockIdx.x * kZWarps + (threadIdx.x >> 5); w < ntask; w += nw) {
+  const int nw = gridDim.x * p.wact;
+  if ((threadIdx.x >> 5) >= p.wact) {   // (no CTA-wide barrier follows)
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // its zeros of W above
+    return;
+  }
+  for (int w = blockIdx.x * p.wact + (threadIdx.x >> 5); w < ntask; w += nw) {
     const bool cv = w * C + grp < p.n_act;       // this group has a column
     const int c = p.cs + (cv ? w * C + grp : 0);
     const int jl = p.jcol[c] - r0;               // >= nt: not a tip
@@ -834,7 +839,14 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     // m = 10000 77.0 -> 74.3 with two, 72.3 with four; bitwise the one-column kernel's results)
     const int cpw = n_act > nsm * kZWarps * 2 ? 4 : 2;
     const int ntask = (n_act + cpw - 1) / cpw;   // warp tasks
-    const int grid = std::max(1, std::min(std::max((ntask + kZWarps - 1) / kZWarps, zb), nsm));   // one 132 KB CTA per SM
+#ifndef ZZ_ZSPREAD
+#define ZZ_ZSPREAD 0
+#endif
+    // warps per CTA that solve: the tasks spread over the SMs first (a chain-bound wavefront) or
+    // packed 16 to a CTA (the other SMs stay with the previous group's update)
+    const bool spread = ZZ_ZSPREAD == 1 || (ZZ_ZSPREAD == 2 && M <= 64);
+    p.wact = spread ? std::max(1, std::min(kZWarps, (ntask + nsm - 1) / nsm)) : kZWarps;
+    const int grid = std::max(1, std::min(std::max((ntask + p.wact - 1) / p.wact, zb), nsm));   // one 132 KB CTA per SM
     if (cpw == 4) k_zdiag<4><<<grid, kZWarps * 32, smem, cs_>>>(p);
     else k_zdiag<2><<<grid, kZWarps * 32, smem, cs_>>>(p);
     ++launches;
