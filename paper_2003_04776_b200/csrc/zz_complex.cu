@@ -839,13 +839,10 @@ extern "C" int zz_ztgevc(int m, const double* S_, int lds, const double* T_, int
     // m = 10000 77.0 -> 74.3 with two, 72.3 with four; bitwise the one-column kernel's results)
     const int cpw = n_act > nsm * kZWarps * 2 ? 4 : 2;
     const int ntask = (n_act + cpw - 1) / cpw;   // warp tasks
-#ifndef ZZ_ZSPREAD
-#define ZZ_ZSPREAD 0
-#endif
-    // warps per CTA that solve: the tasks spread over the SMs first (a chain-bound wavefront) or
-    // packed 16 to a CTA (the other SMs stay with the previous group's update)
-    const bool spread = ZZ_ZSPREAD == 1 || (ZZ_ZSPREAD == 2 && M <= 64);
-    p.wact = spread ? std::max(1, std::min(kZWarps, (ntask + nsm - 1) / nsm)) : kZWarps;
+    // all warps of a CTA solve: the tasks are packed 16 to a CTA, so the other SMs stay with the
+    // previous group's update (spreading them over the SMs first, fewer solving warps per CTA,
+    // was slower from m = 2000: 2.45 -> 2.6 ms, 7.4 -> 8.0 ms at 4000; profiles/r02ap_zspread.txt)
+    p.wact = kZWarps;
     const int grid = std::max(1, std::min(std::max((ntask + p.wact - 1) / p.wact, zb), nsm));   // one 132 KB CTA per SM
     if (cpw == 4) k_zdiag<4><<<grid, kZWarps * 32, smem, cs_>>>(p);
     else k_zdiag<2><<<grid, kZWarps * 32, smem, cs_>>>(p);

@@ -119,7 +119,7 @@ def test_ztgevc_large_sampled(zz, m):
     the others with two."""
     S, T = gen.complex_pencil(m, seed=10)
     X, _ = _run(zz, S, T)
-    cols = [0, 1, 999, 2047, 2048, 3071, m // 2 + 5, m - 1003, m - 2, m - 1]
+    cols = sorted([0, 1, 999, 2047, 2048, 3071, m // 2 + 5, m - 1003, m - 2, m - 1])
     sel = np.zeros(m, np.int32)
     sel[cols] = 1
     ref = oracle.ztgevc(S, T, select=sel)
