@@ -371,7 +371,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
   P.sY = P.e_pend + n;
   P.e_prev = P.sY + n;
   P.e_grp = c->egrp.as<int>();
-  CK(c->nYb.ensure(sizeof(double) * (size_t)n));
+  CK(c->nYb.ensure(sizeof(double) * 2 * (size_t)n));   // two sets: read / written by a group's last decision
   P.nYb = c->nYb.as<double>();
   P.item_col = c->items.as<int>();
   P.real_items = P.item_col + n_items;
@@ -651,6 +651,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
       d2.pack = la;
       d2.team_w = c->diag_team;
       d2.nY_in = dp.nY_in;
+      d2.bnd_in = nyb;   // the recorded bounds alternate between two sets by group (as nY)
       d2.Wout = Wout;
       d2.grp_slot = -1;
       if (fuse_from) {
@@ -739,6 +740,7 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
         for (int k = 1; k < len; ++k) Wg[k] = c->Wx[k - 1].as<double>();
         if (la && gpar == 1)
           for (int k = 0; k < len; ++k) Wg[k] = c->Wy[k].as<double>();
+        bool rest_waited = false;   // the chain has waited for the previous group's bulk update
         for (int sgi = 0; sgi < len; ++sgi) {
           const int X = I - sgi;
           if (sgi > 0 && (r = panel_ready(X))) return r;
@@ -749,7 +751,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
             o.grp_slot = 0;
             o.n_band_reset = len - 2;
             o.use_bound = la && prev_bound;
-            if (la && !prev_bound && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+            if (la && !prev_bound && ev_rest) {
+              CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+              rest_waited = true;
+            }
           } else if (sgi < len - 1) {
             o.fused = 2;
             o.grp_slot = sgi;
@@ -766,9 +771,16 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
             }
             o.zero_pend_end = cs[I + 1];       // tips of the group start from zero pending rows
             o.record_bound = la;
-            // the decision needs the pending maximum of the rows above tile L (the bulk update
-            // of the previous group)
-            if (la && ev_rest) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+            // Lookahead: the decision takes the previous group's recorded bound of the rows
+            // above tile L, as the group's first decision does, so the whole chain of the group
+            // runs beside the previous group's bulk update (it used to wait here for that
+            // update's measured maximum: 0.2-0.5 ms per group with the machine mostly idle).
+            // Without a recorded bound it needs the measured maximum, i.e. that update.
+            o.use_bound = la && prev_bound;
+            if (la && ev_rest && !o.use_bound) {
+              CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+              rest_waited = true;
+            }
           }
           if ((r = diag(X, Wg[sgi], &o))) return r;
           if (sgi < len - 1) {
@@ -809,9 +821,18 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
           // buffer (atomicMax: order-independent), so the next group's last decision reads the
           // maximum over [0, ts[L-1]) exactly as in the plain schedule (base_up(L).max_row)
           fb.max_row = ts[L - 1];
-          if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
+          // the group's W operands and decisions are complete: the bulk may start (after the
+          // previous bulk, in stream order), beside the band part (disjoint rows)
+          // (from m = 4096; on smaller pencils the chain is the critical path and a bulk update
+          // beside its band part slows it: C2 2.05 -> 2.14 ms measured, so there the bulk
+          // starts after the band part)
+          const bool early_bulk = m >= 4096;
           cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
-          CK(cudaEventRecord(ev_dec, ms));
+          if (early_bulk) CK(cudaEventRecord(ev_dec, ms));
+          // the band part updates rows the previous group's bulk update wrote
+          if (ev_rest && !rest_waited) CK(cudaStreamWaitEvent(ms, ev_rest, 0));
+          if ((r = update(fb, ceil_div(ts[L] - (rb & ~1), kBM), ms))) return r;
+          if (!early_bulk) CK(cudaEventRecord(ev_dec, ms));
           CK(cudaStreamWaitEvent(st, ev_dec, 0));
           UpdParams fr = fu;                    // the bulk on the caller's stream
           fr.rows = rb;

@@ -1340,8 +1340,10 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
       const unsigned long long* nyi = P.nY + (long long)p.nY_in * p.n_sel;
       double nyv = 0.0;
       if (c0 >= p.zero_pend_end) {                            // not a tip of the group
-        nyv = __longlong_as_double((long long)nyi[c0]);
-        if (PAIR) nyv = dmaxd(nyv, __longlong_as_double((long long)nyi[c0 + 1]));
+        // (lookahead: the previous group's recorded bound of these rows, at the exponent e_p
+        // it was recorded at, instead of the maximum the bulk update is still measuring)
+        nyv = p.use_bound ? P.nYb[(long long)p.bnd_in * p.n_sel + c0] : __longlong_as_double((long long)nyi[c0]);
+        if (PAIR) nyv = dmaxd(nyv, p.use_bound ? P.nYb[(long long)p.bnd_in * p.n_sel + c0 + 1] : __longlong_as_double((long long)nyi[c0 + 1]));
       }
       const int g0 = min(ep, es);
       double xh = scale2k(lm, g0 - es);
@@ -1362,14 +1364,14 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
         // lookahead: this maximum covers the rows the band and bulk updates measured, which
         // can differ from the plain schedule's; a decision that scales is recomputed without
         // lookahead (as for a group's first decision)
-        if (p.record_bound && ef < g0) atomicOr(&P.status[6], 1);
+        if ((p.record_bound || p.use_bound) && ef < g0) atomicOr(&P.status[6], 1);
         P.sY[c] = ef - e_p;
         P.e_pend[c] = ef;
         P.nY[(long long)(1 - p.nY_in) * p.n_sel + c] = 0ull;
         // lookahead: an upper bound of |pending| after this group's update, at exponent ef
         // (2^(ef-g) (y^ + tau x^), with a margin for the rounding of the sum and the update)
         if (p.record_bound)
-          P.nYb[c] = scale2k(__dmul_rn(__dadd_rn(yh, __dmul_rn(tau, xh)), 1.0 + 0x1p-40), ef - g0);
+          P.nYb[(long long)(1 - p.bnd_in) * p.n_sel + c] = scale2k(__dmul_rn(__dadd_rn(yh, __dmul_rn(tau, xh)), 1.0 + 0x1p-40), ef - g0);
       }
       // each earlier W of this column brought to ef (rare), or zero where the column was not
       // active at that step (stale entries)
@@ -1400,8 +1402,8 @@ __device__ __forceinline__ void solve_task(const Diag2Params& p, const Sm3& sm, 
       double nyv = 0.0;
       if (!tip) {
         // (lookahead: the first step of a group takes the previous group's recorded bound)
-        nyv = p.use_bound ? P.nYb[c0] : __longlong_as_double((long long)nyi[c0]);
-        if (PAIR) nyv = dmaxd(nyv, p.use_bound ? P.nYb[c0 + 1] : __longlong_as_double((long long)nyi[c0 + 1]));
+        nyv = p.use_bound ? P.nYb[(long long)p.bnd_in * p.n_sel + c0] : __longlong_as_double((long long)nyi[c0]);
+        if (PAIR) nyv = dmaxd(nyv, p.use_bound ? P.nYb[(long long)p.bnd_in * p.n_sel + c0 + 1] : __longlong_as_double((long long)nyi[c0 + 1]));
       }
       const int g0 = min(ep, es);
       const double yh = scale2k(nyv, g0 - ep), xh = scale2k(lm, g0 - es);

@@ -152,6 +152,8 @@ struct Diag2Params {
   double* X; long long ldx;
   DevPlan P;
   int nY_in;
+  int bnd_in;        // lookahead: the set of recorded bounds (nYb) this step reads; a group's last
+                     // decision writes the other set
   int cpt;                 // columns per warp task (set by launch_diag3)
   double* Wout;            // where this step's B operand W goes
   // second step of a fused pair (I, J = I - 1): the update of the rows above tile J is done
