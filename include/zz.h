@@ -162,8 +162,8 @@ int zz_set_fusion(int k);
 
 /* Lookahead schedule: the chain of diagonal solves of a step group runs on a high-priority
  * stream beside the bulk of the previous group's update (DESIGN.md s.6 "Lookahead").  The
- * first decision of a group then uses a recorded upper bound of the pending rows instead of
- * their measured maximum; where that bound would make it scale, the call is recomputed
+ * first and the last decision of a group then use a recorded upper bound of the pending rows
+ * instead of their measured maximum; where that bound would make one scale, the call is recomputed
  * without lookahead (zz_info_t.lookahead_redo), so results are always those of the plain
  * schedule, bit for bit.  mode 0 = off, 1 = automatic (default: on for m >= 1024 unless a
  * panel norm exceeds 2^64), 2 = on whenever step groups are used.  Returns 0, -1 or -103. */

@@ -823,10 +823,10 @@ int tgevc_device(Context* c, int m, const double* S, long long lds, const double
           fb.max_row = ts[L - 1];
           // the group's W operands and decisions are complete: the bulk may start (after the
           // previous bulk, in stream order), beside the band part (disjoint rows)
-          // (from m = 4096; on smaller pencils the chain is the critical path and a bulk update
-          // beside its band part slows it: C2 2.05 -> 2.14 ms measured, so there the bulk
-          // starts after the band part)
-          const bool early_bulk = m >= 4096;
+          // (from 4096 columns; with fewer the chain is the critical path and a bulk update
+          // beside its band part slows it -- C2 2.05 -> 2.14 ms, a 1 % subset of C4 45.6 ->
+          // 48.0 ms measured -- so there the bulk starts after the band part)
+          const bool early_bulk = n_sel >= 4096;
           cudaEvent_t ev_dec = c->ev_la[n_la_ev++];
           if (early_bulk) CK(cudaEventRecord(ev_dec, ms));
           // the band part updates rows the previous group's bulk update wrote
